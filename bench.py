@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- GANQ layer quantization (arxiv 2501.12956, Algorithm 1) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One step = the whole hot path for one layer: H = X X^T from the calibration tokens
+(ganq_hessian), then ganq_quantize_layer (precondition, Cholesky, W H, K = 10 x {S-update,
+T-update}).  Workload (BASELINE.json configs[1]): LLaMA-2-7B q_proj, W 4096 x 4096 fp32,
+4-bit, X = 128 x 2048 = 262144 calibration tokens (bf16), K = 10; synthetic seeded data
+(synthetic/, recipe in DESIGN.md).  Metric: rows*iter/s = m * K / layer time.
+
+N > 1 (torchrun, one process per GPU, NCCL): tokens are sharded for H (whole
+GANQ_HESSIAN_CHUNKs per rank), one all-reduce of H, rows sharded m/N per rank
+(strong scaling of one layer); time = max over ranks of the CUDA-event time.
+
+--impl reference runs the fp64 CPU oracle (oracle/, the only baseline this tier has) on a
+bounded sample of the same workload and extrapolates to the layer (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synthetic  # noqa: E402
+
+METRIC = "4096x4096 4-bit layer quantize time (ms), rows·iter/s, % roofline @1/2/4/8"
+UNIT = "rows*iter/s"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return dict(hbm_gbs=d.get("hbm_gbs", 6650.0), bf16=d.get("bf16_tflops", 1590.0),
+                    bf16_sus=d.get("bf16_tflops_sustained", 1400.0), sm_mhz=d.get("sm_max_mhz", 1965.0),
+                    source="measured")
+    return dict(hbm_gbs=6650.0, bf16=1590.0, bf16_sus=1400.0, sm_mhz=1965.0, source="fallback")
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- oracle timing
+def oracle_layer_time(W_rows: np.ndarray, X_bits: np.ndarray, p: int, m: int, nbits: int, K: int):
+    """Time the fp64 oracle on a bounded sample and extrapolate to the full layer.
+
+    H on X_bits (p_s tokens) scaled by p / p_s; Cholesky of the full n x n (preconditioned
+    sample H); K x (S-step, T-step) on the sampled rows scaled by m / rows (rows are
+    independent, Eq. 2).  Returns dict(seconds, value rows*iter/s, sample description)."""
+    import oracle
+    oracle.build()
+    ps, n = X_bits.shape
+    r = W_rows.shape[0]
+    t0 = time.perf_counter()
+    H = oracle.hessian_bf16(X_bits)
+    tH = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Hp, _ = oracle.precondition(H, "adaptive")
+    L = oracle.cholesky(Hp)
+    tC = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    T = oracle.init_codebook(W_rows.astype(np.float32), nbits).astype(np.float64)
+    for _ in range(K):
+        Q, _ = oracle.sstep(W_rows, L, T)
+        T = oracle.tstep(W_rows, Q, H, 1 << nbits)
+    tR = time.perf_counter() - t0
+    total = tH * (p / ps) + tC + tR * (m / r)
+    return dict(seconds=total, value=m * K / total, measured_s=tH + tC + tR,
+                sample=(f"oracle fp64 C (OpenMP): H on {ps} of {p} tokens (x{p / ps:.0f}), full {n}x{n} "
+                        f"Cholesky, K={K} S+T iterations on {r} of {m} rows (x{m / r:.0f}); "
+                        f"extrapolated layer time {total:.1f} s"))
+
+
+def cores():
+    v = os.environ.get("OMP_NUM_THREADS")
+    return int(v) if v else (os.cpu_count() or 1)
+
+
+# --------------------------------------------------------------------------- our arm
+def stage_roofline(name, ms, launches, m, n, p, K, peaks, world):
+    """Algorithmic work of a stage per step."""
+    clk = peaks["sm_mhz"] * 1e6
+    alu_add = 148 * 128 * clk / 1e12          # fp32 adds, TFLOP/s
+    alu_fma = 2 * alu_add                      # fp32 FMA, TFLOP/s
+    fp64 = 148 * 64 * 2 * clk / 1e12           # fp64 FMA, TFLOP/s
+    s = ms / 1e3
+    if s <= 0:
+        return None
+    if name == "hessian":
+        work, unit, bound, peak = n * (n + 1) * p / 1e12, "TFLOP/s", "tensor", peaks["bf16_sus"]
+    elif name == "tstep":
+        work, unit, bound, peak = K * m * n * (n + 1) / 2 / 1e12, "TFLOP/s", "alu", alu_add
+    elif name == "sstep":
+        work, unit, bound, peak = K * m * n * (n - 1) / 1e12, "TFLOP/s", "alu", alu_fma
+    elif name == "gemm_wh":
+        work, unit, bound, peak = 2.0 * m * n * n / 1e12, "TFLOP/s", "alu", alu_fma
+    elif name == "cholesky":
+        work, unit, bound, peak = n ** 3 / 3 / 1e12, "TFLOP/s", "alu", fp64
+    elif name == "precondition":
+        work, unit, bound, peak = 2 * 8 * n * n / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
+    elif name == "derive_operands":
+        work, unit, bound, peak = (8 + 8 + 4 + 4) * n * n / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
+    elif name == "init_codebook":
+        work, unit, bound, peak = 4 * m * n / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
+    else:
+        return None
+    ach = work / s
+    return dict(bound=bound, achieved=round(ach, 3), peak=round(peak, 3), unit=unit, frac=round(ach / peak, 4),
+                ms=round(ms, 4), launches=int(launches))
+
+
+def run_ours(args):
+    from paper_2501_12956_b200 import _lib
+    import paper_2501_12956_b200 as g
+    from paper_2501_12956_b200.dist import shard_rows, shard_tokens
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+    peaks = load_peaks()
+    cfg = synthetic.CONFIGS[args.config]
+    m, n, p, nbits, K = cfg["m"], cfg["n"], cfg["p"], cfg["nbits"], cfg["iters"]
+    r0, r1 = shard_rows(m, world, rank)
+    t0, t1 = shard_tokens(p, world, rank)
+    W = synthetic.make_weights(m, n, seed=1000, device=dev)
+    Xfull = synthetic.make_activations(p, n, seed=2000, device=dev)
+    X = Xfull[t0:t1].contiguous()
+    del Xfull
+    Wl = W[r0:r1].contiguous()
+    ml = r1 - r0
+    H = torch.empty((n, n), dtype=torch.float64, device=dev)
+    Q = torch.empty((ml, n), dtype=torch.uint8, device=dev)
+    T = torch.empty((ml, 1 << nbits), dtype=torch.float32, device=dev)
+
+    def step():
+        g.hessian(X, H=H)
+        if world > 1:
+            dist.all_reduce(H)
+        g.quantize_layer(Wl, H, nbits, K, Q=Q, T=T)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    lib.ganq_profile_enable(1)
+    n0 = int(lib.ganq_launch_count())
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = int(lib.ganq_launch_count()) - n0
+    nst = 12
+    ms_arr = (ctypes_double_array(nst))
+    ln_arr = (ctypes_int64_array(nst))
+    lib.ganq_profile_read(ms_arr, ln_arr, nst)
+    lib.ganq_profile_enable(0)
+    ck = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    value = m * K / (ms_step / 1e3)
+
+    stages = {}
+    for i in range(nst):
+        name = lib.ganq_profile_stage_name(i).decode()
+        if ms_arr[i] <= 0:
+            continue
+        ms_i = ms_arr[i] / args.steps
+        rl = stage_roofline(name, ms_i, ln_arr[i] / args.steps, ml, n, t1 - t0, K, peaks, world)
+        stages[name] = rl if rl else dict(ms=round(ms_i, 4), launches=int(ln_arr[i] / args.steps))
+    dominant = max((k for k in stages if "frac" in stages[k]), key=lambda k: stages[k]["ms"])
+    roof = {k: stages[dominant][k] for k in ("bound", "achieved", "peak", "unit", "frac")}
+    roof["kernel"] = dominant
+    roof["share_of_step"] = round(stages[dominant]["ms"] / ms_step, 4)
+    roof["traffic"] = load_traffic(dominant)
+    roof["peak_source"] = peaks["source"]
+
+    # ---- end to end through the public API with host buffers (pinned), H2D + D2H per step
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        Wh = Wl.cpu().pin_memory()
+        Qh = torch.empty(Q.shape, dtype=Q.dtype).pin_memory()
+        Th = torch.empty(T.shape, dtype=T.dtype).pin_memory()
+        Xd = torch.empty_like(X)
+        Wd = torch.empty_like(Wl)
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            Wd.copy_(Wh, non_blocking=True)
+            g.hessian(Xd, H=H)
+            if world > 1:
+                dist.all_reduce(H)
+            g.quantize_layer(Wd, H, nbits, K, Q=Q, T=T)
+            Qh.copy_(Q, non_blocking=True)
+            Th.copy_(T, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        e2e_step()
+        ks = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(ks):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / ks], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(m * K / (float(te.item()) / 1e3), 3), "unit": UNIT,
+               "ms_per_step": round(float(te.item()), 3),
+               "h2d_bytes_per_step": int(Xh.numel() * Xh.element_size() + Wh.numel() * Wh.element_size()),
+               "d2h_bytes_per_step": int(Qh.numel() * Qh.element_size() + Th.numel() * Th.element_size()),
+               "steps": ks}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows = np.linspace(0, m - 1, 8).astype(int)
+        Wr = W[rows].cpu().numpy().astype(np.float64)
+        Xs = synthetic.bf16_bits(X[:256])
+        ob = oracle_layer_time(Wr, Xs, p, m, nbits, K)
+        cpu = {"value": round(ob["value"], 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
+               "sample": ob["sample"], "measured_s": round(ob["measured_s"], 2)}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+bf16+f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "m": m, "n": n, "n_bits": nbits,
+                       "tokens": p, "iters": K, "rows_per_gpu": ml, "tokens_per_gpu": t1 - t0,
+                       "parallelism": f"tokens+rows x{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (X = 2.15 GB bf16 streamed every step)"},
+            "layer_ms": round(ms_step, 4),
+            "roofline": roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+            "clocks": ck,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_double_array(k):
+    import ctypes
+    return (ctypes.c_double * k)()
+
+
+def ctypes_int64_array(k):
+    import ctypes
+    return (ctypes.c_int64 * k)()
+
+
+def load_traffic(kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        return json.load(open(path)).get(kernel)
+    return None
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    cfg = synthetic.CONFIGS[args.config]
+    m, n, p, nbits, K = cfg["m"], cfg["n"], cfg["p"], cfg["nbits"], cfg["iters"]
+    W = synthetic.make_weights(m, n, seed=1000)
+    rows = np.linspace(0, m - 1, 2).astype(int)
+    Wr = W[rows].numpy().astype(np.float64)
+    X = synthetic.make_activations(128, n, seed=2000)
+    Xs = synthetic.bf16_bits(X)
+    for _ in range(args.warmup):
+        oracle_layer_time(Wr, Xs, p, m, nbits, K)
+    secs = []
+    desc = None
+    for _ in range(args.steps):
+        ob = oracle_layer_time(Wr, Xs, p, m, nbits, K)
+        secs.append(ob["seconds"])
+        desc = ob["sample"]
+    s = sum(secs) / len(secs)
+    value = m * K / s
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": int(os.environ.get("WORLD_SIZE", args.gpus)), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(s * 1e3, 1), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "m": m, "n": n, "n_bits": nbits, "tokens": p,
+                   "iters": K},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2", choices=sorted(synthetic.CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

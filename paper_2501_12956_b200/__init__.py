@@ -1,0 +1,16 @@
+"""GANQ (arxiv 2501.12956) layer-wise LUT quantization solver for B200 (sm_100a).
+
+Public API (torch CUDA tensors; thin binding of include/ganq.h):
+    hessian(X)                         H = X X^T
+    quantize_layer(W, H, n_bits, iters) -> (Q, T)            Algorithm 1
+    objective(W, Q, T, H)              ||WX - W~X||_F^2      Eq. (1)
+    tstep(W, Q, H, n_bits)             closed-form T-update  Eq. (6)
+    factor(H)                          L = chol(H')          Eq. (9) + App. A
+    dist.quantize_layer_distributed    token-sharded H + row-sharded solve over NCCL
+"""
+from .api import (factor, hessian, objective, objective_workspace_size, quantize_layer, tstep,
+                  version, workspace_size)
+from ._lib import GanqError, NotPositiveDefinite
+
+__all__ = ["hessian", "quantize_layer", "objective", "tstep", "factor", "workspace_size",
+           "objective_workspace_size", "version", "GanqError", "NotPositiveDefinite"]

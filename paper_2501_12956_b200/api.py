@@ -1,0 +1,167 @@
+"""Python binding of the GANQ C ABI (include/ganq.h), same names, torch tensors in and out.
+
+Argument marshalling only.  PyTorch provides device memory and the current CUDA stream;
+every step of the method runs in libganq.so's sm_100a kernels.  Inputs must already be
+CUDA tensors of the documented dtype -- there is no CPU path and no silent conversion of
+device placement.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+
+__all__ = ["hessian", "quantize_layer", "objective", "tstep", "factor", "workspace_size",
+           "objective_workspace_size", "version"]
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need(t, dtype, ndim, name):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the GANQ path has no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() != ndim:
+        raise ValueError(f"{name} must be {ndim}-D")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    key = (str(device),)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def version() -> str:
+    return _lib.load().ganq_version().decode()
+
+
+def workspace_size(m: int, n: int, n_bits: int) -> int:
+    return int(_lib.load().ganq_workspace_size(m, n, n_bits))
+
+
+def objective_workspace_size(m: int, n: int) -> int:
+    return int(_lib.load().ganq_objective_workspace_size(m, n))
+
+
+def hessian(X: torch.Tensor, H: torch.Tensor | None = None, accumulate: bool = False, stream=None):
+    """H = X X^T from token-major bf16 activations X (p x n); returns fp64 n x n."""
+    _need(X, torch.bfloat16, 2, "X")
+    p, n = X.shape
+    if H is None:
+        if accumulate:
+            raise ValueError("accumulate=True needs an existing H")
+        H = torch.empty((n, n), dtype=torch.float64, device=X.device)
+    _need(H, torch.float64, 2, "H")
+    lib = _lib.load()
+    _lib.check(lib.ganq_hessian(_ptr(X), p, n, _ptr(H), int(bool(accumulate)), _stream(stream)))
+    return H
+
+
+def _opts(precond, lam, tau, T0, empty_level_rule, trace_buf):
+    o = _lib.Opts()
+    if precond not in _lib.PRECOND:
+        raise ValueError(f"unknown precond {precond!r}")
+    o.precond = _lib.PRECOND[precond]
+    o.empty_level_rule = int(empty_level_rule)
+    o.lam = float(lam)
+    o.tau = float(tau)
+    o.T0 = None if T0 is None else T0.data_ptr()
+    o.obj_trace = trace_buf
+    return o
+
+
+def quantize_layer(W: torch.Tensor, H: torch.Tensor, n_bits: int, iters: int = 10, *,
+                   precond: str = "adaptive", lam: float = 0.0, tau: float = 1e-7,
+                   T0: torch.Tensor | None = None, empty_level_rule: int = 0, trace: bool = False,
+                   Q: torch.Tensor | None = None, T: torch.Tensor | None = None, stream=None):
+    """Algorithm 1 given H: returns (Q uint8 m x n, T fp32 m x 2^N[, obj_trace])."""
+    _need(W, torch.float32, 2, "W")
+    _need(H, torch.float64, 2, "H")
+    m, n = W.shape
+    nlev = 1 << int(n_bits)
+    if Q is None:
+        Q = torch.empty((m, n), dtype=torch.uint8, device=W.device)
+    if T is None:
+        T = torch.empty((m, nlev), dtype=torch.float32, device=W.device)
+    _need(Q, torch.uint8, 2, "Q")
+    _need(T, torch.float32, 2, "T")
+    if T0 is not None:
+        _need(T0, torch.float32, 2, "T0")
+    lib = _lib.load()
+    nbytes = int(lib.ganq_workspace_size(m, n, int(n_bits)))
+    ws = _workspace(nbytes, W.device)
+    tr = (ctypes.c_double * int(iters))() if trace else None
+    o = _opts(precond, lam, tau, T0, empty_level_rule,
+              ctypes.cast(tr, ctypes.POINTER(ctypes.c_double)) if trace else None)
+    _lib.check(lib.ganq_quantize_layer(_ptr(W), m, n, _ptr(H), int(n_bits), int(iters), ctypes.byref(o),
+                                       _ptr(Q), _ptr(T), _ptr(ws), ws.numel(), _stream(stream)))
+    if trace:
+        return Q, T, [float(x) for x in tr]
+    return Q, T
+
+
+def objective(W, Q, T, H, per_row: bool = False, stream=None):
+    """Eq. (1) via Eq. (8) on raw H; returns a Python float (and the fp64 per-row tensor)."""
+    _need(W, torch.float32, 2, "W")
+    _need(Q, torch.uint8, 2, "Q")
+    _need(T, torch.float32, 2, "T")
+    _need(H, torch.float64, 2, "H")
+    m, n = W.shape
+    n_bits = int(T.shape[1]).bit_length() - 1
+    lib = _lib.load()
+    ws = _workspace(int(lib.ganq_objective_workspace_size(m, n)), W.device)
+    out = ctypes.c_double(0.0)
+    pr = torch.empty(m, dtype=torch.float64, device=W.device) if per_row else None
+    _lib.check(lib.ganq_objective(_ptr(W), _ptr(Q), _ptr(T), _ptr(H), m, n, n_bits, ctypes.byref(out),
+                                  _ptr(pr), _ptr(ws), ws.numel(), _stream(stream)))
+    return (out.value, pr) if per_row else out.value
+
+
+def tstep(W, Q, H, n_bits: int, empty_level_rule: int = 0, Tprev=None, stream=None):
+    """T-update alone (Eq. 6) for given codes Q; returns fp32 m x 2^N."""
+    _need(W, torch.float32, 2, "W")
+    _need(Q, torch.uint8, 2, "Q")
+    _need(H, torch.float64, 2, "H")
+    m, n = W.shape
+    T = torch.empty((m, 1 << n_bits), dtype=torch.float32, device=W.device)
+    if Tprev is not None:
+        _need(Tprev, torch.float32, 2, "Tprev")
+    lib = _lib.load()
+    ws = _workspace(int(lib.ganq_workspace_size(m, n, n_bits)), W.device)
+    _lib.check(lib.ganq_tstep(_ptr(W), _ptr(Q), _ptr(H), m, n, int(n_bits), int(empty_level_rule),
+                              _ptr(Tprev), _ptr(T), _ptr(ws), ws.numel(), _stream(stream)))
+    return T
+
+
+def factor(H, precond: str = "adaptive", lam: float = 0.0, tau: float = 1e-7, stream=None):
+    """(L, delta): Cholesky of the preconditioned H (App. A / Remark 1 / Eq. 9)."""
+    _need(H, torch.float64, 2, "H")
+    n = H.shape[0]
+    L = torch.empty_like(H)
+    delta = torch.empty(n, dtype=torch.float64, device=H.device)
+    lib = _lib.load()
+    ws = _workspace(int(lib.ganq_workspace_size(1, n, 1)), H.device)
+    o = _opts(precond, lam, tau, None, 0, None)
+    _lib.check(lib.ganq_factor(_ptr(H), n, ctypes.byref(o), _ptr(L), _ptr(delta), _ptr(ws), ws.numel(),
+                               _stream(stream)))
+    return L, delta

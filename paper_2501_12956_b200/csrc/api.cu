@@ -1,0 +1,458 @@
+// api.cu -- the C ABI declared in include/ganq.h: argument checks, workspace carving and
+// the Algorithm 1 driver.  Every arithmetic step runs in the kernels of
+// hessian.cu, cholesky.cu, sstep.cu, tstep.cu and gemm.cu.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <vector>
+
+#include "ganq_internal.cuh"
+
+namespace ganq {
+
+static thread_local char g_msg[512] = "";
+static thread_local int64_t g_index = -1;
+
+void set_error(ganq_status_t, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_msg, sizeof g_msg, fmt, ap);
+  va_end(ap);
+  g_index = -1;
+}
+void set_error_index(int64_t idx) { g_index = idx; }
+ganq_status_t cuda_fail(cudaError_t e, const char* where) {
+  set_error(GANQ_ERR_CUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e),
+            where);
+  return GANQ_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- instrumentation
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+enum Stage {
+  ST_HESSIAN = 0, ST_PRECOND, ST_CHOLESKY, ST_DERIVE, ST_GEMM_WH, ST_INIT, ST_SSTEP, ST_TGRAM,
+  ST_OBJECTIVE, ST_COPY, ST_TSTEP_ONLY, ST_FACTOR_COPY, ST_COUNT
+};
+static const char* kStageNames[ST_COUNT] = {
+    "hessian", "precondition", "cholesky", "derive_operands", "gemm_wh", "init_codebook",
+    "sstep", "tstep", "objective", "copy", "tstep_api", "factor_copy"};
+static_assert(ST_COUNT == GANQ_PROFILE_STAGES, "stage table");
+
+struct Prof {
+  bool on = false;
+  struct Rec { int stage; cudaEvent_t a, b; int64_t launches; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double ms[ST_COUNT] = {};
+  int64_t launches[ST_COUNT] = {};
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+static thread_local Prof g_prof;
+
+struct StageScope {
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  int64_t l0;
+  StageScope(int s, cudaStream_t stream) : stage(s), st(stream), l0(g_launches.load()) {
+    if (g_prof.on) { a = g_prof.get(); cudaEventRecord(a, st); }
+  }
+  ~StageScope() {
+    if (g_prof.on && a) {
+      cudaEvent_t b = g_prof.get();
+      cudaEventRecord(b, st);
+      g_prof.recs.push_back({stage, a, b, g_launches.load() - l0});
+    }
+  }
+};
+#define GANQ_STAGE(s) StageScope _stage_scope_##__LINE__(s, st)
+
+namespace {
+
+struct Layout {
+  size_t A64, Lhat, H32, WH, E, EH, G, b, cnt, fb, status, mean, per_row, total_d, end;
+};
+
+Layout make_layout(int64_t m, int64_t n, int nlev) {
+  Layout L{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const size_t nn = (size_t)n * (size_t)n, mn = (size_t)m * (size_t)n;
+  L.A64 = take(nn * sizeof(double));
+  L.Lhat = take(nn * sizeof(float));
+  L.H32 = take(nn * sizeof(float));
+  L.WH = take(mn * sizeof(float));
+  L.E = take(mn * sizeof(float));
+  L.EH = take(mn * sizeof(float));
+  L.G = take((size_t)m * nlev * nlev * sizeof(double));
+  L.b = take((size_t)m * nlev * sizeof(double));
+  L.cnt = take((size_t)m * nlev * sizeof(int));
+  L.fb = take((size_t)m * sizeof(int));
+  L.status = take(sizeof(int));
+  L.mean = take(sizeof(double));
+  L.per_row = take((size_t)m * sizeof(double));
+  L.total_d = take(sizeof(double));
+  L.end = off;
+  return L;
+}
+
+template <typename T>
+T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + off);
+}
+
+ganq_status_t check_shape(int64_t m, int64_t n, int n_bits) {
+  if (m < 1 || n < 1) {
+    set_error(GANQ_ERR_INVALID_ARG, "m = %lld and n = %lld must be >= 1", (long long)m, (long long)n);
+    return GANQ_ERR_INVALID_ARG;
+  }
+  if (n_bits < 1 || n_bits > 8) {
+    set_error(GANQ_ERR_INVALID_ARG, "n_bits = %d outside [1, 8]", n_bits);
+    return GANQ_ERR_INVALID_ARG;
+  }
+  if (n_bits > 4) {
+    set_error(GANQ_ERR_UNSUPPORTED, "n_bits = %d: this build supports N <= 4 (2^N <= 16 levels)",
+              n_bits);
+    return GANQ_ERR_UNSUPPORTED;
+  }
+  if (n > (int64_t)1 << 20 || m > (int64_t)1 << 26) {
+    set_error(GANQ_ERR_UNSUPPORTED, "shape too large (m = %lld, n = %lld)", (long long)m,
+              (long long)n);
+    return GANQ_ERR_UNSUPPORTED;
+  }
+  return GANQ_OK;
+}
+
+ganq_status_t check_opts(const ganq_opts_t& o) {
+  if (o.precond < 0 || o.precond > 2) {
+    set_error(GANQ_ERR_INVALID_ARG, "unknown preconditioning policy %d", o.precond);
+    return GANQ_ERR_INVALID_ARG;
+  }
+  if (o.precond == GANQ_PRECOND_FIXED_LAMBDA && !(o.lambda > 0.0)) {
+    set_error(GANQ_ERR_INVALID_ARG, "FIXED_LAMBDA needs lambda > 0 (got %g)", o.lambda);
+    return GANQ_ERR_INVALID_ARG;
+  }
+  if (o.precond == GANQ_PRECOND_ADAPTIVE && !(o.tau >= 0.0)) {
+    set_error(GANQ_ERR_INVALID_ARG, "ADAPTIVE needs tau >= 0 (got %g)", o.tau);
+    return GANQ_ERR_INVALID_ARG;
+  }
+  if (o.empty_level_rule != 0 && o.empty_level_rule != 1) {
+    set_error(GANQ_ERR_INVALID_ARG, "empty_level_rule must be 0 or 1");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  return GANQ_OK;
+}
+
+// Preconditioned factor into ws.A64; reports NOT_PD (synchronises the stream).
+ganq_status_t factor(const double* H, int64_t n, const ganq_opts_t& o, void* ws, const Layout& L,
+                     double* delta, cudaStream_t st) {
+  double* A = at<double>(ws, L.A64);
+  int* status = at<int>(ws, L.status);
+  ganq_status_t s;
+  {
+    GANQ_STAGE(ST_PRECOND);
+    s = launch_precondition(H, n, o.precond, o.lambda, o.tau, A, delta, at<double>(ws, L.mean), st);
+    if (s) return s;
+  }
+  GANQ_CUDA_TRY(cudaMemsetAsync(status, 0x7f, sizeof(int), st));
+  {
+    GANQ_STAGE(ST_CHOLESKY);
+    if ((s = launch_cholesky(A, n, status, st))) return s;
+  }
+  int h_status = 0;
+  GANQ_CUDA_TRY(cudaMemcpyAsync(&h_status, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GANQ_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_status < n) {
+    set_error(GANQ_ERR_NOT_PD, "cholesky: non-positive pivot at %d", h_status);
+    set_error_index(h_status);
+    return GANQ_ERR_NOT_PD;
+  }
+  return GANQ_OK;
+}
+
+// f = sum_i e_i H32 e_i^T with E, EH, per_row scratch; result left in ws.total_d (device).
+ganq_status_t objective_device(const float* W, const uint8_t* Q, const float* T, const float* H32,
+                               int64_t m, int64_t n, int nlev, float* E, float* EH, double* per_row,
+                               double* total, cudaStream_t st) {
+  ganq_status_t s;
+  GANQ_STAGE(ST_OBJECTIVE);
+  if ((s = launch_residual(W, Q, T, m, n, nlev, E, st))) return s;
+  if ((s = launch_gemm_f32(E, H32, EH, m, n, n, st))) return s;
+  if ((s = launch_rowdot(E, EH, m, n, per_row, st))) return s;
+  return launch_sum(per_row, m, total, st);
+}
+
+}  // namespace
+}  // namespace ganq
+
+using namespace ganq;
+
+extern "C" {
+
+void ganq_default_opts(ganq_opts_t* o) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->precond = GANQ_PRECOND_ADAPTIVE;
+  o->empty_level_rule = 0;
+  o->lambda = 0.0;
+  o->tau = 1e-7;
+  o->T0 = nullptr;
+  o->obj_trace = nullptr;
+}
+
+int ganq_profile_enable(int on) {
+  for (auto& r : g_prof.recs) { g_prof.pool.push_back(r.a); g_prof.pool.push_back(r.b); }
+  g_prof.recs.clear();
+  for (int i = 0; i < ST_COUNT; ++i) { g_prof.ms[i] = 0.0; g_prof.launches[i] = 0; }
+  g_prof.on = on != 0;
+  return 0;
+}
+
+int ganq_profile_read(double* ms, int64_t* launches, int max_stages) {
+  for (auto& r : g_prof.recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) == cudaSuccess && cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess)
+      g_prof.ms[r.stage] += t;
+    g_prof.launches[r.stage] += r.launches;
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.recs.clear();
+  const int k = max_stages < ST_COUNT ? max_stages : ST_COUNT;
+  for (int i = 0; i < k; ++i) {
+    if (ms) ms[i] = g_prof.ms[i];
+    if (launches) launches[i] = g_prof.launches[i];
+  }
+  return ST_COUNT;
+}
+
+const char* ganq_profile_stage_name(int stage) {
+  return (stage >= 0 && stage < ST_COUNT) ? kStageNames[stage] : "";
+}
+
+int64_t ganq_launch_count(void) { return g_launches.load(); }
+
+const char* ganq_last_error(void) { return g_msg; }
+int64_t ganq_last_error_index(void) { return g_index; }
+const char* ganq_version(void) { return "ganq-b200 0.1 (sm_100a)"; }
+
+ganq_status_t ganq_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate,
+                           void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (p < 1 || n < 1 || !X || !H) {
+    set_error(GANQ_ERR_INVALID_ARG, "ganq_hessian: p = %lld, n = %lld must be >= 1 and pointers set",
+              (long long)p, (long long)n);
+    return GANQ_ERR_INVALID_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  GANQ_STAGE(ST_HESSIAN);
+  return launch_hessian(X, p, n, H, accumulate, st);
+}
+
+size_t ganq_workspace_size(int64_t m, int64_t n, int n_bits) {
+  if (m < 1 || n < 1 || n_bits < 1 || n_bits > 8) return 0;
+  return make_layout(m, n, 1 << n_bits).end;
+}
+
+ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const double* H, int n_bits,
+                                  int iters, const ganq_opts_t* opts, uint8_t* Q, float* T,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  ganq_status_t s;
+  if ((s = check_shape(m, n, n_bits))) return s;
+  if (iters < 1) {
+    set_error(GANQ_ERR_INVALID_ARG, "iters = %d must be >= 1", iters);
+    return GANQ_ERR_INVALID_ARG;
+  }
+  if (!W || !H || !Q || !T) {
+    set_error(GANQ_ERR_INVALID_ARG, "null W/H/Q/T");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  ganq_opts_t o;
+  ganq_default_opts(&o);
+  if (opts) o = *opts;
+  if ((s = check_opts(o))) return s;
+  const int nlev = 1 << n_bits;
+  const Layout L = make_layout(m, n, nlev);
+  if (!workspace || workspace_bytes < L.end) {
+    set_error(GANQ_ERR_WORKSPACE, "workspace of %zu bytes < required %zu", workspace_bytes, L.end);
+    return GANQ_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  void* ws = workspace;
+  // H' = precondition(H), L = Cholesky(H')   (App. A / Remark 1, Eq. 9)
+  if ((s = factor(H, n, o, ws, L, nullptr, st))) return s;
+  float* Lhat = at<float>(ws, L.Lhat);
+  float* H32 = at<float>(ws, L.H32);
+  float* WH = at<float>(ws, L.WH);
+  float* E = at<float>(ws, L.E);
+  float* EH = at<float>(ws, L.EH);
+  {
+    GANQ_STAGE(ST_DERIVE);
+    if ((s = launch_derive_operands(at<double>(ws, L.A64), H, n, Lhat, H32, st))) return s;
+  }
+  {
+    // W H (fixed across iterations: W_i H S_i^T of Eq. 6)
+    GANQ_STAGE(ST_GEMM_WH);
+    if ((s = launch_gemm_f32(W, H32, WH, m, n, n, st))) return s;
+  }
+  {
+    // T^0 (reading R-6)
+    GANQ_STAGE(ST_INIT);
+    if (o.T0) {
+      GANQ_CUDA_TRY(cudaMemcpyAsync(T, o.T0, sizeof(float) * (size_t)m * nlev, cudaMemcpyDeviceToDevice, st));
+    } else if ((s = launch_init_codebook(W, m, n, nlev, T, st))) {
+      return s;
+    }
+  }
+  GANQ_CUDA_TRY(cudaMemsetAsync(at<int>(ws, L.fb), 0, sizeof(int) * (size_t)m, st));
+  for (int k = 0; k < iters; ++k) {
+    {
+      // S-update
+      GANQ_STAGE(ST_SSTEP);
+      if ((s = launch_sstep(W, Lhat, T, m, n, nlev, Q, E, st))) return s;
+    }
+    {
+      // T-update, raw H (reading R-4)
+      GANQ_STAGE(ST_TGRAM);
+      if ((s = launch_tstep(WH, Q, H32, m, n, nlev, o.empty_level_rule, T, at<double>(ws, L.G),
+                            at<double>(ws, L.b), at<int>(ws, L.cnt), at<int>(ws, L.fb), st)))
+        return s;
+    }
+    if (o.obj_trace) {
+      if ((s = objective_device(W, Q, T, H32, m, n, nlev, E, EH, at<double>(ws, L.per_row),
+                                at<double>(ws, L.total_d), st)))
+        return s;
+      GANQ_CUDA_TRY(cudaMemcpyAsync(&o.obj_trace[k], at<double>(ws, L.total_d), sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
+      GANQ_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+  }
+  GANQ_LAUNCH_CHECK("ganq_quantize_layer");
+  return GANQ_OK;
+}
+
+size_t ganq_objective_workspace_size(int64_t m, int64_t n) {
+  if (m < 1 || n < 1) return 0;
+  size_t off = 0;
+  off = align_up(off + (size_t)n * n * sizeof(float), 256);      // H32
+  off = align_up(off + (size_t)m * n * sizeof(float), 256);      // E
+  off = align_up(off + (size_t)m * n * sizeof(float), 256);      // EH
+  off = align_up(off + (size_t)m * sizeof(double), 256);         // per_row
+  off = align_up(off + sizeof(double), 256);                     // total
+  return off;
+}
+
+ganq_status_t ganq_objective(const float* W, const uint8_t* Q, const float* T, const double* H,
+                             int64_t m, int64_t n, int n_bits, double* out, double* per_row,
+                             void* workspace, size_t workspace_bytes, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  ganq_status_t s;
+  if ((s = check_shape(m, n, n_bits))) {
+    if (s != GANQ_ERR_UNSUPPORTED) return s;  // the objective itself supports any N <= 8
+  }
+  if (!W || !Q || !T || !H || !out) {
+    set_error(GANQ_ERR_INVALID_ARG, "null argument");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  const size_t need = ganq_objective_workspace_size(m, n);
+  if (!workspace || workspace_bytes < need) {
+    set_error(GANQ_ERR_WORKSPACE, "workspace of %zu bytes < required %zu", workspace_bytes, need);
+    return GANQ_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  size_t off = 0;
+  float* H32 = at<float>(workspace, off);
+  off = align_up(off + (size_t)n * n * sizeof(float), 256);
+  float* E = at<float>(workspace, off);
+  off = align_up(off + (size_t)m * n * sizeof(float), 256);
+  float* EH = at<float>(workspace, off);
+  off = align_up(off + (size_t)m * n * sizeof(float), 256);
+  double* pr = at<double>(workspace, off);
+  off = align_up(off + (size_t)m * sizeof(double), 256);
+  double* tot = at<double>(workspace, off);
+  {
+    GANQ_STAGE(ST_DERIVE);
+    if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
+  }
+  if ((s = objective_device(W, Q, T, H32, m, n, 1 << n_bits, E, EH, per_row ? per_row : pr, tot, st)))
+    return s;
+  GANQ_CUDA_TRY(cudaMemcpyAsync(out, tot, sizeof(double), cudaMemcpyDeviceToHost, st));
+  GANQ_CUDA_TRY(cudaStreamSynchronize(st));
+  return GANQ_OK;
+}
+
+ganq_status_t ganq_tstep(const float* W, const uint8_t* Q, const double* H, int64_t m, int64_t n,
+                         int n_bits, int empty_level_rule, const float* Tprev, float* T,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  ganq_status_t s;
+  if ((s = check_shape(m, n, n_bits))) return s;
+  if (empty_level_rule != 0 && empty_level_rule != 1) {
+    set_error(GANQ_ERR_INVALID_ARG, "empty_level_rule must be 0 or 1");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  const int nlev = 1 << n_bits;
+  const Layout L = make_layout(m, n, nlev);
+  if (!workspace || workspace_bytes < L.end) {
+    set_error(GANQ_ERR_WORKSPACE, "workspace of %zu bytes < required %zu", workspace_bytes, L.end);
+    return GANQ_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  float* H32 = at<float>(workspace, L.H32);
+  float* WH = at<float>(workspace, L.WH);
+  GANQ_STAGE(ST_TSTEP_ONLY);
+  if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
+  if ((s = launch_gemm_f32(W, H32, WH, m, n, n, st))) return s;
+  if (empty_level_rule == 1 && Tprev && Tprev != T)
+    GANQ_CUDA_TRY(cudaMemcpyAsync(T, Tprev, sizeof(float) * (size_t)m * nlev, cudaMemcpyDeviceToDevice, st));
+  GANQ_CUDA_TRY(cudaMemsetAsync(at<int>(workspace, L.fb), 0, sizeof(int) * (size_t)m, st));
+  return launch_tstep(WH, Q, H32, m, n, nlev, empty_level_rule, T, at<double>(workspace, L.G),
+                      at<double>(workspace, L.b), at<int>(workspace, L.cnt), at<int>(workspace, L.fb),
+                      st);
+}
+
+ganq_status_t ganq_factor(const double* H, int64_t n, const ganq_opts_t* opts, double* Lout,
+                          double* delta, void* workspace, size_t workspace_bytes, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  ganq_status_t s;
+  if ((s = check_shape(1, n, 1))) return s;
+  if (!H || !Lout) {
+    set_error(GANQ_ERR_INVALID_ARG, "null H/L");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  ganq_opts_t o;
+  ganq_default_opts(&o);
+  if (opts) o = *opts;
+  if ((s = check_opts(o))) return s;
+  const Layout L = make_layout(1, n, 2);
+  if (!workspace || workspace_bytes < L.end) {
+    set_error(GANQ_ERR_WORKSPACE, "workspace of %zu bytes < required %zu", workspace_bytes, L.end);
+    return GANQ_ERR_WORKSPACE;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((s = factor(H, n, o, workspace, L, delta, st))) return s;
+  GANQ_CUDA_TRY(cudaMemcpyAsync(Lout, at<double>(workspace, L.A64), sizeof(double) * (size_t)n * n,
+                                cudaMemcpyDeviceToDevice, st));
+  return GANQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+"""C-ABI library checks that need no GPU: it builds for sm_100a, loads, exports every
+symbol include/ganq.h declares, and rejects invalid arguments before touching CUDA."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2501_12956_b200 import _lib
+from paper_2501_12956_b200 import build as gbuild
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ganq.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ganq_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    gbuild.build()
+    return _lib.load()
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for s in ("ganq_hessian", "ganq_quantize_layer", "ganq_objective", "ganq_workspace_size",
+              "ganq_last_error"):
+        assert s in syms
+
+
+def test_exports_every_declared_symbol(lib):
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert set(declared_symbols()) == set(_lib.SIG), "binding signatures must cover the header exactly"
+
+
+def test_sm100a_code_in_library(lib):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in out
+
+
+def test_tensor_core_and_tma_instructions_present(lib):
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", _lib.LIB_PATH],
+                          capture_output=True, text=True, check=True).stdout
+    assert "UTCHMMA" in sass or "UTCQMMA" in sass or "UTCMMA" in sass  # tcgen05.mma
+    assert "UTMALDG" in sass  # TMA tile loads
+    assert "LDTM" in sass  # tcgen05.ld
+
+
+def test_workspace_size(lib):
+    assert lib.ganq_workspace_size(0, 10, 4) == 0
+    assert lib.ganq_workspace_size(10, 10, 9) == 0
+    a = lib.ganq_workspace_size(64, 128, 3)
+    b = lib.ganq_workspace_size(128, 128, 3)
+    assert 0 < a < b
+    assert lib.ganq_workspace_size(4096, 4096, 4) > 4096 * 4096 * (8 + 4 + 4)
+
+
+def test_argument_errors_without_gpu(lib):
+    P = ctypes.c_void_p(1)
+    st = lib.ganq_quantize_layer(P, 0, 4, P, 4, 10, None, P, P, P, 10, None)
+    assert st == _lib.ERR_INVALID_ARG and b"must be >= 1" in lib.ganq_last_error()
+    st = lib.ganq_quantize_layer(P, 4, 4, P, 0, 10, None, P, P, P, 10, None)
+    assert st == _lib.ERR_INVALID_ARG
+    st = lib.ganq_quantize_layer(P, 4, 4, P, 6, 10, None, P, P, P, 10, None)
+    assert st == _lib.ERR_UNSUPPORTED
+    st = lib.ganq_quantize_layer(P, 4, 4, P, 4, 0, None, P, P, P, 10, None)
+    assert st == _lib.ERR_INVALID_ARG
+    o = _lib.Opts()
+    lib.ganq_default_opts(ctypes.byref(o))
+    assert o.precond == 0 and o.tau == pytest.approx(1e-7)
+    o.precond = 1
+    o.lam = 0.0
+    st = lib.ganq_quantize_layer(P, 4, 4, P, 2, 1, ctypes.byref(o), P, P, P, 10, None)
+    assert st == _lib.ERR_INVALID_ARG and b"lambda" in lib.ganq_last_error()
+    o.precond = 0
+    st = lib.ganq_quantize_layer(P, 4, 4, P, 2, 1, ctypes.byref(o), P, P, None, 0, None)
+    assert st == _lib.ERR_WORKSPACE
+    st = lib.ganq_hessian(P, 0, 8, P, 0, None)
+    assert st == _lib.ERR_INVALID_ARG
+
+
+def test_binding_rejects_cpu_tensors():
+    import torch
+    import paper_2501_12956_b200 as g
+    with pytest.raises(ValueError, match="CUDA"):
+        g.hessian(torch.zeros((4, 8), dtype=torch.bfloat16))
+    with pytest.raises(ValueError, match="CUDA"):
+        g.quantize_layer(torch.zeros((4, 8)), torch.zeros((8, 8), dtype=torch.float64), 2, 1)
