@@ -79,7 +79,7 @@ struct StageScope {
 namespace {
 
 struct Layout {
-  size_t A64, Lhat, H32, WH, E, EH, G, b, cnt, fb, status, mean, per_row, total_d, end;
+  size_t A64, Lhat, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, status, mean, per_row, total_d, end;
 };
 
 Layout make_layout(int64_t m, int64_t n, int nlev) {
@@ -98,9 +98,13 @@ Layout make_layout(int64_t m, int64_t n, int nlev) {
   L.E = take(mn * sizeof(float));
   L.EH = take(mn * sizeof(float));
   L.G = take((size_t)m * nlev * nlev * sizeof(double));
+  L.Dv = take((size_t)m * nlev * sizeof(double));
   L.b = take((size_t)m * nlev * sizeof(double));
   L.cnt = take((size_t)m * nlev * sizeof(int));
   L.fb = take((size_t)m * sizeof(int));
+  const size_t P = (size_t)tq_pitch(n);
+  L.Hq = take(3 * P * P);
+  L.qscale = take(P * sizeof(double));
   L.status = take(sizeof(int));
   L.mean = take(sizeof(double));
   L.per_row = take((size_t)m * sizeof(double));
@@ -307,6 +311,11 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
     if ((s = launch_derive_operands(at<double>(ws, L.A64), H, n, Lhat, H32, st))) return s;
   }
   {
+    // fixed-point int8 digits of H's strict lower triangle for the tensor-core T-update
+    GANQ_STAGE(ST_DERIVE);
+    if ((s = launch_tq_prep(H, n, at<int8_t>(ws, L.Hq), at<double>(ws, L.qscale), st))) return s;
+  }
+  {
     // W H (fixed across iterations: W_i H S_i^T of Eq. 6)
     GANQ_STAGE(ST_GEMM_WH);
     if ((s = launch_gemm_f32(W, H32, WH, m, n, n, st))) return s;
@@ -330,7 +339,8 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
     {
       // T-update, raw H (reading R-4)
       GANQ_STAGE(ST_TGRAM);
-      if ((s = launch_tstep(WH, Q, H32, m, n, nlev, o.empty_level_rule, T, at<double>(ws, L.G),
+      if ((s = launch_tstep(H, at<int8_t>(ws, L.Hq), at<double>(ws, L.qscale), WH, Q, m, n, nlev,
+                            o.empty_level_rule, T, at<double>(ws, L.G), at<double>(ws, L.Dv),
                             at<double>(ws, L.b), at<int>(ws, L.cnt), at<int>(ws, L.fb), st)))
         return s;
     }
@@ -420,11 +430,14 @@ ganq_status_t ganq_tstep(const float* W, const uint8_t* Q, const double* H, int6
   float* WH = at<float>(workspace, L.WH);
   GANQ_STAGE(ST_TSTEP_ONLY);
   if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
+  if ((s = launch_tq_prep(H, n, at<int8_t>(workspace, L.Hq), at<double>(workspace, L.qscale), st)))
+    return s;
   if ((s = launch_gemm_f32(W, H32, WH, m, n, n, st))) return s;
   if (empty_level_rule == 1 && Tprev && Tprev != T)
     GANQ_CUDA_TRY(cudaMemcpyAsync(T, Tprev, sizeof(float) * (size_t)m * nlev, cudaMemcpyDeviceToDevice, st));
   GANQ_CUDA_TRY(cudaMemsetAsync(at<int>(workspace, L.fb), 0, sizeof(int) * (size_t)m, st));
-  return launch_tstep(WH, Q, H32, m, n, nlev, empty_level_rule, T, at<double>(workspace, L.G),
+  return launch_tstep(H, at<int8_t>(workspace, L.Hq), at<double>(workspace, L.qscale), WH, Q, m, n, nlev,
+                      empty_level_rule, T, at<double>(workspace, L.G), at<double>(workspace, L.Dv),
                       at<double>(workspace, L.b), at<int>(workspace, L.cnt), at<int>(workspace, L.fb),
                       st);
 }

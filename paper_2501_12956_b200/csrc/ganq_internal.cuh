@@ -43,9 +43,14 @@ ganq_status_t launch_derive_operands(const double* L, const double* H, int64_t n
 // tstep.cu
 ganq_status_t launch_init_codebook(const float* W, int64_t m, int64_t n, int nlev, float* T,
                                    cudaStream_t st);
-ganq_status_t launch_tstep(const float* WH, const uint8_t* Q, const float* H32, int64_t m, int64_t n,
-                           int nlev, int empty_rule, float* T, double* G, double* b, int* cnt,
-                           int* fallback, cudaStream_t st);
+ganq_status_t launch_tstep(const double* H, const int8_t* Hq, const double* qscale, const float* WH,
+                           const uint8_t* Q, int64_t m, int64_t n, int nlev, int empty_rule, float* T,
+                           double* G, double* Dv, double* b, int* cnt, int* fallback, cudaStream_t st);
+// tgram_tc.cu
+int64_t tq_pitch(int64_t n);
+ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* scale, cudaStream_t st);
+ganq_status_t launch_tgram_tc(const int8_t* Hq, const double* scale, const uint8_t* Q, int64_t m,
+                              int64_t n, int nlev, double* Cg, cudaStream_t st);
 // sstep.cu
 ganq_status_t launch_sstep(const float* W, const float* Lhat, const float* T, int64_t m, int64_t n,
                            int nlev, uint8_t* Q, float* E, cudaStream_t st);
@@ -161,6 +166,37 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+// 32 lanes x 32 bit, 32 consecutive columns per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+// D[tmem] (+)= A * B with signed int8 operands and exact int32 accumulation (kind::i8).
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Make generic-proxy shared-memory writes visible to the async proxy (tensor core / TMA).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -188,6 +224,10 @@ __host__ __device__ constexpr uint32_t umma_idesc(uint32_t ab_format, uint32_t a
                                                   uint32_t b_mn_major, uint32_t M, uint32_t N) {
   return (1u << 4) | (ab_format << 7) | (ab_format << 10) | (a_mn_major << 15) |
          (b_mn_major << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+// kind::i8: signed int8 A and B (format 1), S32 accumulator (c_format 2), K-major operands.
+__host__ __device__ constexpr uint32_t umma_idesc_s8(uint32_t M, uint32_t N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 #endif
 

@@ -6,14 +6,9 @@
 // built without materialising S_i (one-hot segmented sums): by symmetry
 //     G_i = C_i + C_i^T + D_i,   C_i[a][b] = sum_{j>k} [q_ij=a][q_ik=b] H_jk,
 //                                D_i[a][a] = sum_j [q_ij=a] H_jj.
-// Kernel tgram: one warp per row, 8 rows per CTA sharing 32 x 128 tiles of H (fp32,
-// strict lower part) staged in shared memory.  Lanes own 4 consecutive columns k
-// (float4); for each level a the warp walks the j's of the tile whose code is a
-// (ballot mask, warp-uniform), so a sits in a static register index: acc[a][v] += H[j][k_v].
-// After a 128-column chunk, acc[a][v] is scattered to the bin b_v = q_ik by a
-// deterministic shuffle reduction into fp64 accumulators (no atomics: bitwise
-// reproducible).  RHS b_i[a] = sum_j [q_ij=a] (W H)_ij and the level counts come from the
-// same kernel.  Kernel tsolve: one warp per row, Cholesky of the 2^N x 2^N system in fp64
+// C comes from the tensor-core kernel in tgram_tc.cu; kernel trhs gives D, the right-hand
+// side b_i[a] = sum_j [q_ij=a] (W H)_ij and the level counts (one warp per row, fp64).
+// Kernel tsolve: one warp per row, Cholesky of the 2^N x 2^N system in fp64
 // (unused levels get an identity row -> T = 0, Moore-Penrose, reading R-9); rows whose
 // used block is numerically singular fall back to a Jacobi eigen pseudo-inverse.
 #include "ganq_internal.cuh"
@@ -21,142 +16,32 @@
 namespace ganq {
 namespace {
 
-constexpr int KC = 128;  // columns k per chunk (32 lanes x float4)
-constexpr int JT = 32;   // rows j per H tile
-constexpr int WARPS = 8; // rows per CTA
-
-// Sum 16 (or fewer) per-lane bin values across the warp by recursive halving.
-// In: v[NB] per lane.  Out: returns the full warp sum of bin `bin_of_lane(lane)`.
-template <int NB>
-__device__ __forceinline__ float halving_reduce(float (&v)[NB], int lane) {
-  // step with offset 16, 8, ... while more than one bin remains
-  int nb = NB;
-  int off = 16;
-#pragma unroll
-  for (int step = 0; (1 << step) < NB; ++step) {
-    const int half = NB >> (step + 1);
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int q = 0; q < half; ++q) {
-      // lanes with bit `off` clear keep bins [0, half), others keep [half, 2*half)
-      const float send = upper ? v[q] : v[q + half];
-      const float keep = upper ? v[q + half] : v[q];
-      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-    off >>= 1;
-    nb = half;
-  }
-  float s = v[0];
-  for (; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  (void)nb;
-  return s;
-}
-// Bin held by `lane` after halving_reduce<NB>: bits 4,3,... of lane (msb first) select halves.
-template <int NB>
-__device__ __forceinline__ int bin_of_lane(int lane) {
-  int bin = 0;
-  int off = 16;
-#pragma unroll
-  for (int step = 0; (1 << step) < NB; ++step) {
-    const int half = NB >> (step + 1);
-    if (lane & off) bin += half;
-    off >>= 1;
-  }
-  return bin;
-}
-
+// Per row (one warp): D_i[a] = sum_j [q_ij=a] H_jj, b_i[a] = sum_j [q_ij=a] (W H)_ij and the
+// level counts (fp64 accumulation; lanes over j, warp-shuffle reduction in fixed order).
 template <int NLEV>
-__global__ void __launch_bounds__(WARPS * 32)
-tgram_kernel(const float* __restrict__ H32, const float* __restrict__ WH, const uint8_t* __restrict__ Q,
-             int64_t m, int64_t n, double* __restrict__ G, double* __restrict__ bvec,
-             int* __restrict__ cnt) {
-  __shared__ __align__(16) float Hs[JT][KC];
-  __shared__ double Cs[WARPS][NLEV][NLEV + 1];
+__global__ void __launch_bounds__(256)
+trhs_kernel(const double* __restrict__ H, const float* __restrict__ WH, const uint8_t* __restrict__ Q,
+            int64_t m, int64_t n, double* __restrict__ Dv, double* __restrict__ bvec,
+            int* __restrict__ cnt) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * WARPS + warp;
-  const bool live = row < m;
-  const uint8_t* q = Q + (live ? row : 0) * n;
-
-  double gacc[NLEV];  // this lane's bin (bin_of_lane) column of C, all a
-#pragma unroll
-  for (int a = 0; a < NLEV; ++a) gacc[a] = 0.0;
-  const int mybin = bin_of_lane<NLEV>(lane);
-
-  const int64_t nchunks = (n + KC - 1) / KC;
-  for (int64_t kc = 0; kc < nchunks; ++kc) {
-    const int64_t k0 = kc * KC + 4 * lane;
-    int bk[4];
-#pragma unroll
-    for (int v = 0; v < 4; ++v) bk[v] = (live && k0 + v < n) ? (int)q[k0 + v] : -1;
-    float acc[NLEV][4];
-#pragma unroll
-    for (int a = 0; a < NLEV; ++a)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[a][v] = 0.0f;
-
-    for (int64_t j0 = kc * KC; j0 < n; j0 += JT) {  // tiles with some j > k
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < JT * KC / 4; idx += WARPS * 32) {
-        const int jj = idx / (KC / 4), kk = (idx % (KC / 4)) * 4;
-        const int64_t j = j0 + jj;
-        float4 h;
-        float* hp = reinterpret_cast<float*>(&h);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int64_t k = kc * KC + kk + v;
-          hp[v] = (j < n && k < n && j > k) ? H32[j * n + k] : 0.0f;
-        }
-        *reinterpret_cast<float4*>(&Hs[jj][kk]) = h;
-      }
-      __syncthreads();
-      const int64_t jl = j0 + lane;
-      const int qj = (live && jl < n) ? (int)q[jl] : -1;
-#pragma unroll
-      for (int a = 0; a < NLEV; ++a) {
-        unsigned msk = __ballot_sync(0xffffffffu, qj == a);
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        while (msk) {
-          const int jj = __ffs(msk) - 1;
-          msk &= msk - 1;
-          const float4 h = *reinterpret_cast<const float4*>(&Hs[jj][4 * lane]);
-          s0 += h.x; s1 += h.y; s2 += h.z; s3 += h.w;
-        }
-        acc[a][0] += s0; acc[a][1] += s1; acc[a][2] += s2; acc[a][3] += s3;
-      }
-    }
-    // scatter acc[a][v] to bins b = bk[v] and reduce over the warp (deterministic)
-#pragma unroll
-    for (int a = 0; a < NLEV; ++a) {
-      float binv[NLEV];
-#pragma unroll
-      for (int b = 0; b < NLEV; ++b) binv[b] = 0.0f;
-#pragma unroll
-      for (int v = 0; v < 4; ++v)
-#pragma unroll
-        for (int b = 0; b < NLEV; ++b) binv[b] += (bk[v] == b) ? acc[a][v] : 0.0f;
-      const float s = halving_reduce<NLEV>(binv, lane);
-      gacc[a] += (double)s;
-    }
-  }
-
-  // diagonal part D, the right-hand side b and the level counts (lanes over j)
+  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  if (row >= m) return;
+  const uint8_t* q = Q + row * n;
+  const float* wh = WH + row * n;
   double dsum[NLEV], rsum[NLEV];
   int c[NLEV];
 #pragma unroll
   for (int a = 0; a < NLEV; ++a) { dsum[a] = 0.0; rsum[a] = 0.0; c[a] = 0; }
-  if (live) {
-    const float* wh = WH + row * n;
-    for (int64_t j = lane; j < n; j += 32) {
-      const int qj = q[j];
-      const double hd = (double)H32[j * n + j];
-      const double r = (double)wh[j];
+  for (int64_t j = lane; j < n; j += 32) {
+    const int qj = q[j];
+    const double hd = H[j * n + j];
+    const double r = (double)wh[j];
 #pragma unroll
-      for (int a = 0; a < NLEV; ++a) {
-        const bool hit = qj == a;
-        dsum[a] += hit ? hd : 0.0;
-        rsum[a] += hit ? r : 0.0;
-        c[a] += hit ? 1 : 0;
-      }
+    for (int a = 0; a < NLEV; ++a) {
+      const bool hit = qj == a;
+      dsum[a] += hit ? hd : 0.0;
+      rsum[a] += hit ? r : 0.0;
+      c[a] += hit ? 1 : 0;
     }
   }
 #pragma unroll
@@ -167,31 +52,12 @@ tgram_kernel(const float* __restrict__ H32, const float* __restrict__ WH, const 
       c[a] += __shfl_xor_sync(0xffffffffu, c[a], o);
     }
   }
-  // assemble G = C + C^T + D
-  const bool writer = (NLEV >= 32) ? true : ((lane & ((32 / NLEV) - 1)) == 0);
-  if (writer) {
+  if (lane == 0) {
 #pragma unroll
-    for (int a = 0; a < NLEV; ++a) Cs[warp][a][mybin] = gacc[a];
-  }
-  __syncwarp();
-  if (live) {
-    double* g = G + row * NLEV * NLEV;
-    for (int idx = lane; idx < NLEV * NLEV; idx += 32) {
-      const int a = idx / NLEV, b = idx % NLEV;
-      double v = Cs[warp][a][b] + Cs[warp][b][a];
-      if (a == b) {
-#pragma unroll
-        for (int aa = 0; aa < NLEV; ++aa)
-          if (aa == a) v += dsum[aa];
-      }
-      g[idx] = v;
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int a = 0; a < NLEV; ++a) {
-        bvec[row * NLEV + a] = rsum[a];
-        cnt[row * NLEV + a] = c[a];
-      }
+    for (int a = 0; a < NLEV; ++a) {
+      Dv[row * NLEV + a] = dsum[a];
+      bvec[row * NLEV + a] = rsum[a];
+      cnt[row * NLEV + a] = c[a];
     }
   }
 }
@@ -199,8 +65,9 @@ tgram_kernel(const float* __restrict__ H32, const float* __restrict__ WH, const 
 // One warp per row; lane l < NLEV holds row l of the (regularised) system.
 template <int NLEV>
 __global__ void __launch_bounds__(256)
-tsolve_kernel(const double* __restrict__ G, const double* __restrict__ bvec, const int* __restrict__ cnt,
-              int64_t m, int empty_rule, float* __restrict__ T, int* __restrict__ fallback) {
+tsolve_kernel(double* __restrict__ G, const double* __restrict__ Dv, const double* __restrict__ bvec,
+              const int* __restrict__ cnt, int64_t m, int empty_rule, float* __restrict__ T,
+              int* __restrict__ fallback) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * 8 + warp;
   if (row >= m) return;
@@ -208,11 +75,19 @@ tsolve_kernel(const double* __restrict__ G, const double* __restrict__ bvec, con
   const bool used = cnt[row * NLEV + l] > 0;
   double g[NLEV];
   double maxdiag = 0.0;
+  // assemble G = C + C^T + D (C holds the strict lower sums j > k)
+#pragma unroll
+  for (int c = 0; c < NLEV; ++c)
+    g[c] = G[(row * NLEV + l) * NLEV + c] + G[(row * NLEV + c) * NLEV + l] + (c == l ? Dv[row * NLEV + l] : 0.0);
+  __syncwarp();
+  if (lane < NLEV) {
+#pragma unroll
+    for (int c = 0; c < NLEV; ++c) G[(row * NLEV + l) * NLEV + c] = g[c];  // full G for the pinv path
+  }
 #pragma unroll
   for (int c = 0; c < NLEV; ++c) {
-    const double v = G[(row * NLEV + l) * NLEV + c];
     const bool usedc = __shfl_sync(0xffffffffu, used ? 1 : 0, c) != 0;
-    g[c] = (used && usedc) ? v : ((c == l && !used) ? 1.0 : 0.0);
+    g[c] = (used && usedc) ? g[c] : ((c == l && !used) ? 1.0 : 0.0);
   }
 #pragma unroll
   for (int c = 0; c < NLEV; ++c) {
@@ -357,13 +232,14 @@ __global__ void init_codebook_kernel(const float* __restrict__ W, int64_t m, int
 }
 
 template <int NLEV>
-ganq_status_t launch_tstep_t(const float* WH, const uint8_t* Q, const float* H32, int64_t m, int64_t n,
-                             int empty_rule, float* T, double* G, double* b, int* cnt, int* fb,
-                             cudaStream_t st) {
-  tgram_kernel<NLEV><<<(unsigned)((m + WARPS - 1) / WARPS), WARPS * 32, 0, st>>>(H32, WH, Q, m, n, G,
-                                                                                 b, cnt);
-  GANQ_LAUNCH_CHECK("tgram_kernel");
-  tsolve_kernel<NLEV><<<(unsigned)((m + 7) / 8), 256, 0, st>>>(G, b, cnt, m, empty_rule, T, fb);
+ganq_status_t launch_tstep_t(const double* H, const int8_t* Hq, const double* qscale, const float* WH,
+                             const uint8_t* Q, int64_t m, int64_t n, int empty_rule, float* T, double* G,
+                             double* Dv, double* b, int* cnt, int* fb, cudaStream_t st) {
+  ganq_status_t s = launch_tgram_tc(Hq, qscale, Q, m, n, NLEV, G, st);
+  if (s) return s;
+  trhs_kernel<NLEV><<<(unsigned)((m + 7) / 8), 256, 0, st>>>(H, WH, Q, m, n, Dv, b, cnt);
+  GANQ_LAUNCH_CHECK("trhs_kernel");
+  tsolve_kernel<NLEV><<<(unsigned)((m + 7) / 8), 256, 0, st>>>(G, Dv, b, cnt, m, empty_rule, T, fb);
   GANQ_LAUNCH_CHECK("tsolve_kernel");
   tsolve_pinv_kernel<NLEV><<<(unsigned)((m + 127) / 128), 128, 0, st>>>(G, b, cnt, m, empty_rule, T,
                                                                          fb);
@@ -380,14 +256,14 @@ ganq_status_t launch_init_codebook(const float* W, int64_t m, int64_t n, int nle
   return GANQ_OK;
 }
 
-ganq_status_t launch_tstep(const float* WH, const uint8_t* Q, const float* H32, int64_t m, int64_t n,
-                           int nlev, int empty_rule, float* T, double* G, double* b, int* cnt,
-                           int* fb, cudaStream_t st) {
+ganq_status_t launch_tstep(const double* H, const int8_t* Hq, const double* qscale, const float* WH,
+                           const uint8_t* Q, int64_t m, int64_t n, int nlev, int empty_rule, float* T,
+                           double* G, double* Dv, double* b, int* cnt, int* fb, cudaStream_t st) {
   switch (nlev) {
-    case 2: return launch_tstep_t<2>(WH, Q, H32, m, n, empty_rule, T, G, b, cnt, fb, st);
-    case 4: return launch_tstep_t<4>(WH, Q, H32, m, n, empty_rule, T, G, b, cnt, fb, st);
-    case 8: return launch_tstep_t<8>(WH, Q, H32, m, n, empty_rule, T, G, b, cnt, fb, st);
-    case 16: return launch_tstep_t<16>(WH, Q, H32, m, n, empty_rule, T, G, b, cnt, fb, st);
+    case 2: return launch_tstep_t<2>(H, Hq, qscale, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 4: return launch_tstep_t<4>(H, Hq, qscale, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 8: return launch_tstep_t<8>(H, Hq, qscale, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 16: return launch_tstep_t<16>(H, Hq, qscale, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
     default:
       set_error(GANQ_ERR_UNSUPPORTED, "tstep: 2^N = %d levels unsupported (N must be 1..4)", nlev);
       return GANQ_ERR_UNSUPPORTED;
