@@ -79,7 +79,8 @@ struct StageScope {
 namespace {
 
 struct Layout {
-  size_t A64, Lhat, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, status, mean, per_row, total_d, end;
+  size_t A64, Lhat, LThi, LTlo, Ehi, Elo, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, status, mean,
+      per_row, total_d, end;
 };
 
 Layout make_layout(int64_t m, int64_t n, int nlev) {
@@ -92,7 +93,12 @@ Layout make_layout(int64_t m, int64_t n, int nlev) {
   };
   const size_t nn = (size_t)n * (size_t)n, mn = (size_t)m * (size_t)n;
   L.A64 = take(nn * sizeof(double));
-  L.Lhat = take(nn * sizeof(float));
+  const size_t np = (size_t)ss_pitch(n);
+  L.Lhat = take((size_t)n * np * sizeof(float));
+  L.LThi = take((size_t)n * np * sizeof(float));
+  L.LTlo = take((size_t)n * np * sizeof(float));
+  L.Ehi = take((size_t)m * np * sizeof(float));
+  L.Elo = take((size_t)m * np * sizeof(float));
   L.H32 = take(nn * sizeof(float));
   L.WH = take(mn * sizeof(float));
   L.E = take(mn * sizeof(float));
@@ -308,7 +314,10 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
   float* EH = at<float>(ws, L.EH);
   {
     GANQ_STAGE(ST_DERIVE);
-    if ((s = launch_derive_operands(at<double>(ws, L.A64), H, n, Lhat, H32, st))) return s;
+    if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
+    if ((s = launch_lhat_split(at<double>(ws, L.A64), n, Lhat, at<float>(ws, L.LThi), at<float>(ws, L.LTlo),
+                               st)))
+      return s;
   }
   {
     // fixed-point int8 digits of H's strict lower triangle for the tensor-core T-update
@@ -334,7 +343,9 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
     {
       // S-update
       GANQ_STAGE(ST_SSTEP);
-      if ((s = launch_sstep(W, Lhat, T, m, n, nlev, Q, E, st))) return s;
+      if ((s = launch_sstep_tc(W, Lhat, at<float>(ws, L.LThi), at<float>(ws, L.LTlo), T, m, n, nlev, Q,
+                               at<float>(ws, L.Ehi), at<float>(ws, L.Elo), st)))
+        return s;
     }
     {
       // T-update, raw H (reading R-4)

@@ -51,9 +51,13 @@ int64_t tq_pitch(int64_t n);
 ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* scale, cudaStream_t st);
 ganq_status_t launch_tgram_tc(const int8_t* Hq, const double* scale, const uint8_t* Q, int64_t m,
                               int64_t n, int nlev, double* Cg, cudaStream_t st);
-// sstep.cu
-ganq_status_t launch_sstep(const float* W, const float* Lhat, const float* T, int64_t m, int64_t n,
-                           int nlev, uint8_t* Q, float* E, cudaStream_t st);
+// sstep_tc.cu
+int64_t ss_pitch(int64_t n);
+ganq_status_t launch_lhat_split(const double* L, int64_t n, float* Lhat, float* LThi, float* LTlo,
+                                cudaStream_t st);
+ganq_status_t launch_sstep_tc(const float* W, const float* Lhat, const float* LThi, const float* LTlo,
+                              const float* T, int64_t m, int64_t n, int nlev, uint8_t* Q, float* Ehi,
+                              float* Elo, cudaStream_t st);
 // gemm.cu
 ganq_status_t launch_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N,
                               int64_t K, cudaStream_t st);

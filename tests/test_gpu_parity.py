@@ -160,6 +160,25 @@ def test_sstep_teacher_forced(m, n, p, nbits, policy):
         Tk = Tn
 
 
+@pytest.mark.parametrize("n", [131, 1, 2, 258])
+def test_sstep_teacher_forced_unaligned_n(n):
+    """n not a multiple of 4/32/128: right-aligned TMA storage, phantom panel columns."""
+    m, nbits = 37, 3
+    rng = np.random.default_rng(n)
+    Xt = rng.normal(size=(4 * n + 8, n)) * np.exp(0.3 * rng.normal(size=n))
+    Xb = torch.from_numpy(Xt.astype(np.float32)).to(torch.bfloat16)
+    Hn = oracle.hessian_bf16(synthetic.bf16_bits(Xb))  # host H (ganq_hessian needs n % 8 == 0)
+    H = torch.from_numpy(Hn).to(DEV)
+    W = synthetic.make_weights(m, n, seed=n)
+    L = oracle.cholesky(oracle.precondition(Hn, "adaptive")[0])
+    Tk = torch.from_numpy(oracle.init_codebook(W.numpy(), nbits)).to(DEV)
+    for k in range(3):
+        Qg, Tn = g.quantize_layer(W.to(DEV), H, nbits, 1, T0=Tk)
+        mism, bad, _ = audit(W.numpy(), L, Tk.cpu().numpy(), Qg.cpu().numpy())
+        assert bad == 0 and mism <= max(2, 0.001 * m * n)
+        Tk = Tn
+
+
 # ----------------------------------------------------------------------------- P-4 T-step
 
 @pytest.mark.parametrize("m,n,p,nbits,rule", [(64, 128, 256, 3, 0), (80, 192, 4000, 4, 0),
