@@ -39,9 +39,8 @@ template <int NLEV>
 struct TcSmem {
   static constexpr int R = 128 / NLEV;
   alignas(16) float stage[128][33];          // combined Dt chunk (32 j) per (i,b) row
-  alignas(16) uint8_t cq[R][TK];             // codes of the current k-tile (producers)
   alignas(16) uint8_t perm[R][TJ];           // per (row, 32-chunk): local j sorted by code
-  alignas(16) double scale[TJ];              // s_j of the current j-tile
+  alignas(16) float scale[TJ];               // s_j of the current j-tile (fp32)
   alignas(16) uint8_t off[R][4][NLEV + 1];   // segment offsets per (row, chunk, level)
   alignas(8) uint64_t full[MAX_STAGES], empty[MAX_STAGES], tfull, tempty;
   uint32_t tmem_slot;
@@ -50,7 +49,7 @@ struct TcSmem {
 template <int NLEV>
 __global__ void __launch_bounds__(THREADS, 1)
 tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ Q,
-                const double* __restrict__ scale, int64_t m, int64_t n, int64_t P,
+                const double* __restrict__ scale, int64_t m, int64_t n, int64_t P, int jsplit,
                 double* __restrict__ Cg) {
   constexpr int R = 128 / NLEV;
   constexpr int STAGES = kStages<NLEV>;
@@ -60,8 +59,13 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   TcSmem<NLEV>& sm = *reinterpret_cast<TcSmem<NLEV>*>(tiles + STAGES * STAGE_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r0 = (int64_t)blockIdx.x * R;
+  const int64_t r0 = (int64_t)(blockIdx.x >> 1) * R;
   const int NT = (int)((n + TJ - 1) / TJ);
+  // Two CTAs per row group: j-tiles [0, jsplit) and [jsplit, NT) (balanced triangle work);
+  // each writes its own partial C (summed in fixed order by the solve kernel).
+  const int half = blockIdx.x & 1;
+  const int jt_lo = half ? jsplit : 0, jt_hi = half ? NT : jsplit;
+  double* Cpart = Cg + (size_t)half * (size_t)m * NLEV * NLEV;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);
@@ -83,7 +87,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     // ---------------- TMA: three digit tiles of H per stage
     if (lane == 0) {
       uint32_t ks = 0;
-      for (int jt = 0; jt < NT; ++jt)
+      for (int jt = jt_lo; jt < jt_hi; ++jt)
         for (int kt = 0; kt <= jt; ++kt, ++ks) {
           const uint32_t s = ks % STAGES;
           mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
@@ -98,8 +102,8 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     // ---------------- MMA issuer
     if (lane == 0) {
       uint32_t ks = 0;
-      for (int jt = 0; jt < NT; ++jt) {
-        mbar_wait(&sm.tempty, (jt & 1) ^ 1);
+      for (int jt = jt_lo; jt < jt_hi; ++jt) {
+        mbar_wait(&sm.tempty, ((jt - jt_lo) & 1) ^ 1);
         tc_fence_after();
         for (int kt = 0; kt <= jt; ++kt, ++ks) {
           const uint32_t s = ks % STAGES;
@@ -122,48 +126,65 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       }
     }
   } else if (warp < 4) {
-    // ---------------- one-hot producers: A[(i,b)][k] = [q_ik == b] (int8), K-major SW128
+    // ---------------- one-hot producers: A[(i,b)][k] = [q_ik == b] (int8), K-major SW128.
+    // Thread pt owns (row i, 16-column chunk c) pairs and writes the NLEV one-hot rows of
+    // each; its 16 code bytes are loaded one k-tile ahead (no shared staging, no barriers).
     const int pt = threadIdx.x - 64;  // 0..63
-    uint32_t ks = 0;
-    for (int jt = 0; jt < NT; ++jt)
-      for (int kt = 0; kt <= jt; ++kt, ++ks) {
-        const uint32_t s = ks % STAGES;
-        // stage the k-tile's codes (out of range -> 0xFF, matches no level)
-        for (int idx = pt; idx < R * (TK / 16); idx += NPROD) {
-          const int i = idx / (TK / 16), c = idx % (TK / 16);
-          const int64_t row = r0 + i, k = (int64_t)kt * TK + c * 16;
-          uint4 v = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-          if (row < m) {
-            const uint8_t* src = Q + row * n + k;
-            if (k + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-              v = *reinterpret_cast<const uint4*>(src);
-            } else {
-              uint8_t* vb = reinterpret_cast<uint8_t*>(&v);
+    constexpr int PAIRS = R * (TK / 16) / NPROD;  // (i, c) pairs per thread = 16 / NLEV
+    auto load_codes = [&](int kt, uint4 (&v)[PAIRS]) {
 #pragma unroll
-              for (int q = 0; q < 16; ++q) vb[q] = (k + q < n) ? src[q] : (uint8_t)0xFF;
-            }
+      for (int u = 0; u < PAIRS; ++u) {
+        const int pr = pt + NPROD * u;
+        const int i = pr / (TK / 16), c = pr % (TK / 16);
+        const int64_t row = r0 + i, k = (int64_t)kt * TK + c * 16;
+        v[u] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        if (row < m) {
+          const uint8_t* src = Q + row * n + k;
+          if (k + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            v[u] = __ldg(reinterpret_cast<const uint4*>(src));
+          } else {
+            uint8_t* vb = reinterpret_cast<uint8_t*>(&v[u]);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) vb[q] = (k + q < n) ? src[q] : (uint8_t)0xFF;
           }
-          *reinterpret_cast<uint4*>(&sm.cq[i][c * 16]) = v;
         }
-        named_bar_sync(2, NPROD);
-        mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
-        uint8_t* A = tiles + s * STAGE_BYTES;
-        for (int idx = pt; idx < 128 * (TK / 16); idx += NPROD) {
-          const int rr = idx / (TK / 16), c = idx % (TK / 16);
-          const int i = rr / NLEV, b = rr % NLEV;
-          const uint4 codes = *reinterpret_cast<const uint4*>(&sm.cq[i][c * 16]);
+      }
+    };
+    uint4 cur[PAIRS], nxt[PAIRS];
+    int jt = jt_lo, kt = 0;
+    if (jt < jt_hi) load_codes(kt, cur);
+    uint32_t ks = 0;
+    while (jt < jt_hi) {
+      const uint32_t s = ks % STAGES;
+      int jn = jt, kn = kt + 1;
+      if (kn > jn) { ++jn; kn = 0; }
+      if (jn < jt_hi) load_codes(kn, nxt);  // prefetch the next k-tile's codes
+      mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
+      uint8_t* A = tiles + s * STAGE_BYTES;
+#pragma unroll
+      for (int u = 0; u < PAIRS; ++u) {
+        const int pr = pt + NPROD * u;
+        const int i = pr / (TK / 16), c = pr % (TK / 16);
+#pragma unroll
+        for (int b = 0; b < NLEV; ++b) {
+          const int rr = i * NLEV + b;
           const uint32_t bb = 0x01010101u * (uint32_t)b;
           uint4 o;
-          o.x = __vcmpeq4(codes.x, bb) & 0x01010101u;
-          o.y = __vcmpeq4(codes.y, bb) & 0x01010101u;
-          o.z = __vcmpeq4(codes.z, bb) & 0x01010101u;
-          o.w = __vcmpeq4(codes.w, bb) & 0x01010101u;
+          o.x = __vcmpeq4(cur[u].x, bb) & 0x01010101u;
+          o.y = __vcmpeq4(cur[u].y, bb) & 0x01010101u;
+          o.z = __vcmpeq4(cur[u].z, bb) & 0x01010101u;
+          o.w = __vcmpeq4(cur[u].w, bb) & 0x01010101u;
           *reinterpret_cast<uint4*>(A + rr * 128 + ((c ^ (rr & 7)) << 4)) = o;
         }
-        fence_proxy_async_smem();
-        mbar_arrive(&sm.full[s]);
-        named_bar_sync(2, NPROD);  // cq is rewritten for the next k-tile
       }
+      fence_proxy_async_smem();
+      mbar_arrive(&sm.full[s]);
+#pragma unroll
+      for (int u = 0; u < PAIRS; ++u) cur[u] = nxt[u];
+      jt = jn;
+      kt = kn;
+      ++ks;
+    }
   } else {
     // ---------------- epilogue: exact integer sums -> fp32 values -> sorted segmented walk
     const int et = threadIdx.x - 128;      // 0..127 == TMEM lane == (i, b)
@@ -173,7 +194,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     double acc[NLEV];
 #pragma unroll
     for (int a = 0; a < NLEV; ++a) acc[a] = 0.0;
-    for (int jt = 0; jt < NT; ++jt) {
+    for (int jt = jt_lo; jt < jt_hi; ++jt) {
       const int64_t J0 = (int64_t)jt * TJ;
       // sorted order of each row's 32-column chunks of this j-tile (counting sort by code)
       for (int task = quarter; task < R * 4; task += 4) {
@@ -192,9 +213,9 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         if (lane == 0) sm.off[ri][c][NLEV] = (uint8_t)base;
         if (pos >= 0) sm.perm[ri][c * 32 + pos] = (uint8_t)lane;
       }
-      if (et < TJ) sm.scale[et] = (J0 + et < n) ? scale[J0 + et] : 0.0;
+      if (et < TJ) sm.scale[et] = (J0 + et < n) ? (float)scale[J0 + et] : 0.0f;
       named_bar_sync(1, 128);
-      mbar_wait(&sm.tfull, jt & 1);
+      mbar_wait(&sm.tfull, (jt - jt_lo) & 1);
       tc_fence_after();
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
@@ -206,18 +227,19 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         tmem_ld_wait();
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
-          const double v = ((double)(int)d0[t] * 65536.0 + (double)(int)d1[t] * 256.0 +
-                            (double)(int)d2[t]) * sm.scale[c * 32 + t];
-          sm.stage[et][t] = (float)v;
+          // exact int32 digit sums -> fp32 value (one rounding per step, ~2^-24 relative)
+          const float v = fmaf((float)(int)d0[t], 65536.0f,
+                               fmaf((float)(int)d1[t], 256.0f, (float)(int)d2[t]));
+          sm.stage[et][t] = v * sm.scale[c * 32 + t];
         }
         __syncwarp();
         // only this thread's own stage row is read below: no CTA-wide barrier needed
 #pragma unroll
         for (int a = 0; a < NLEV; ++a) {
           const int s0 = sm.off[i][c][a], s1 = sm.off[i][c][a + 1];
-          double s = 0.0;
-          for (int q = s0; q < s1; ++q) s += (double)sm.stage[et][sm.perm[i][c * 32 + q]];
-          acc[a] += s;
+          float s = 0.0f;
+          for (int q = s0; q < s1; ++q) s += sm.stage[et][sm.perm[i][c * 32 + q]];
+          acc[a] += (double)s;
         }
         __syncwarp();
       }
@@ -229,7 +251,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     const int64_t row = r0 + i;
     if (row < m) {
 #pragma unroll
-      for (int a = 0; a < NLEV; ++a) Cg[(row * NLEV + a) * NLEV + b] = acc[a];
+      for (int a = 0; a < NLEV; ++a) Cpart[(row * NLEV + a) * NLEV + b] = acc[a];
     }
   }
   tc_fence_before();
@@ -308,7 +330,14 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   const size_t smem = 1024 + kStages<NLEV> * STAGE_BYTES + sizeof(TcSmem<NLEV>);
   GANQ_CUDA_TRY(cudaFuncSetAttribute(tgram_tc_kernel<NLEV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-  tgram_tc_kernel<NLEV><<<(unsigned)((m + R - 1) / R), THREADS, smem, st>>>(tmap, Q, scale, m, n, P, Cg);
+  // split the triangle of j-tiles (work of tile jt ~ jt + 1) into two halves of equal work
+  const int NT = (int)((n + TJ - 1) / TJ);
+  const int64_t total = (int64_t)NT * (NT + 1) / 2;
+  int jsplit = 0;
+  int64_t acc = 0;
+  while (jsplit < NT && 2 * (acc + jsplit + 1) <= total) acc += ++jsplit;
+  const unsigned groups = (unsigned)((m + R - 1) / R);
+  tgram_tc_kernel<NLEV><<<2 * groups, THREADS, smem, st>>>(tmap, Q, scale, m, n, P, jsplit, Cg);
   GANQ_LAUNCH_CHECK("tgram_tc_kernel");
   return GANQ_OK;
 }

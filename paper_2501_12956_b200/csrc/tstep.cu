@@ -75,10 +75,15 @@ tsolve_kernel(double* __restrict__ G, const double* __restrict__ Dv, const doubl
   const bool used = cnt[row * NLEV + l] > 0;
   double g[NLEV];
   double maxdiag = 0.0;
-  // assemble G = C + C^T + D (C holds the strict lower sums j > k)
+  // assemble G = C + C^T + D; C (strict lower sums j > k) arrives as two partials
+  // (j-tile halves, tgram_tc.cu) in G[0..m) and G[m..2m), added in fixed order
+  const double* G2 = G + (size_t)m * NLEV * NLEV;
 #pragma unroll
-  for (int c = 0; c < NLEV; ++c)
-    g[c] = G[(row * NLEV + l) * NLEV + c] + G[(row * NLEV + c) * NLEV + l] + (c == l ? Dv[row * NLEV + l] : 0.0);
+  for (int c = 0; c < NLEV; ++c) {
+    const double clc = G[(row * NLEV + l) * NLEV + c] + G2[(row * NLEV + l) * NLEV + c];
+    const double ccl = G[(row * NLEV + c) * NLEV + l] + G2[(row * NLEV + c) * NLEV + l];
+    g[c] = clc + ccl + (c == l ? Dv[row * NLEV + l] : 0.0);
+  }
   __syncwarp();
   if (lane < NLEV) {
 #pragma unroll
