@@ -66,7 +66,11 @@ def quantize_layer_distributed(W: torch.Tensor, X_local: torch.Tensor, n_bits: i
         quantize_fn = quantize_fn or api.quantize_layer
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    H = hessian_fn(X_local)
+    n = W.shape[1]
+    if X_local.shape[0] == 0:  # more ranks than token chunks: this rank contributes nothing
+        H = torch.zeros((n, n), dtype=torch.float64, device=W.device)
+    else:
+        H = hessian_fn(X_local)
     if world > 1:
         dist.all_reduce(H, op=dist.ReduceOp.SUM, group=group)
     m = W.shape[0]
