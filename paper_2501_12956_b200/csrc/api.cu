@@ -103,7 +103,7 @@ Layout make_layout(int64_t m, int64_t n, int nlev) {
   L.WH = take(mn * sizeof(float));
   L.E = take(mn * sizeof(float));
   L.EH = take(mn * sizeof(float));
-  L.G = take(2 * (size_t)m * nlev * nlev * sizeof(double));  // two partial C's (tgram_tc halves)
+  L.G = take(4 * (size_t)m * nlev * nlev * sizeof(double));  // 4 partial C's (tgram_tc split)
   L.Dv = take((size_t)m * nlev * sizeof(double));
   L.b = take((size_t)m * nlev * sizeof(double));
   L.cnt = take((size_t)m * nlev * sizeof(int));

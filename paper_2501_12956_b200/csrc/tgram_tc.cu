@@ -3,17 +3,23 @@
 //   G_i = S_i H S_i^T = C_i + C_i^T + D_i,   C_i[a][b] = sum_{j>k} [q_ij=a][q_ik=b] H_jk
 //
 // (P:143-144 batches the T-update over rows; the sums over the one-hot S_i are m n^2 / 2
-// additions per iteration, the largest term of the loop.)  We compute, for a group of
-// R = 128 / 2^N rows (M = 128 pairs (i, b)),
+// additions per iteration, the largest term of the loop.)  For a group of R = 128 / 2^N rows
+// (M = 128 pairs (i, b)) we compute
 //     Dt[(i,b)][j] = sum_{k<j} [q_ik = b] * H_jk            (tensor cores, int8 x int8 -> int32)
 //     C_i[a][b]   += sum_j [q_ij = a] * Dt[(i,b)][j]          (sorted segmented walk, fp64)
 // H's strict lower triangle is stored once per layer as 24-bit fixed point per row j
 // (scale s_j = max_{k<j}|H_jk| / (2^23 - 2^16)) split into three balanced int8 digits
 // (reading R-14), so the tensor-core sums are EXACT integers: the result is deterministic and
-// independent of summation order.  The one-hot operand [q_ik = b] is generated in shared
-// memory from the codes, in the canonical K-major 128B-swizzled UMMA layout; the digit
-// tiles of H arrive by TMA.  One CTA per row group: warp 0 = TMA, warp 1 = MMA issuer
-// (+TMEM owner), warps 2-3 = one-hot producers, warps 4-7 = epilogue (TMEM lane quarter each).
+// independent of summation order.
+//
+// Pipeline (one CTA per (row group, j range); SPLIT CTAs per group over balanced j ranges):
+//   warp 0     TMA: the three digit tiles of H (128 j x 64 k, SWIZZLE_64B) per stage
+//   warp 1     MMA issuer (+TMEM owner): 3 int32 accumulators of 128 columns
+//   warps 2-3  one-hot producers: A[(i,b)][k] = [q_ik == b] in the K-major SW64 layout,
+//              codes prefetched one stage ahead
+//   warps 4-7  epilogue: drain TMEM (digits -> fp32 * s_j) into a shared staging tile and
+//              release the accumulators at once, then the sorted walk overlaps the next
+//              j-tile's MMAs
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -25,47 +31,60 @@ namespace ganq {
 namespace {
 
 constexpr int TJ = 128;          // j per tile (UMMA N)
-constexpr int TK = 128;          // k per stage (one 128-byte swizzle row of int8)
-constexpr int MAX_STAGES = 3;
-template <int NLEV> constexpr int kStages = (NLEV == 2) ? 2 : 3;  // smem budget
-constexpr int TILE_BYTES = 128 * TK;             // 16 KB (one int8 operand tile)
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;      // A (one-hot) + 3 digit tiles of H
+constexpr int TK = 64;           // k per stage (64-byte swizzle rows of int8)
+constexpr int STAGES = 4;
+constexpr int A_TILE = 128 * TK;                 // 8 KB one-hot operand
+constexpr int B_TILE = TJ * TK;                  // 8 KB digit tile of H
+constexpr int STAGE_BYTES = A_TILE + 3 * B_TILE; // 32 KB
+constexpr int SPLIT = 4;                         // CTAs per row group (balanced j ranges)
 constexpr int THREADS = 256;
 constexpr int NPROD = 64;                        // one-hot producer threads (warps 2-3)
+constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile (sorting unit)
 constexpr uint32_t IDESC = umma_idesc_s8(128, TJ);
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
+
+// SW64 K-major UMMA descriptor: 64-byte rows, 8-row atoms of 512 B (SBO), layout type 4.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
 
 template <int NLEV>
 struct TcSmem {
   static constexpr int R = 128 / NLEV;
-  alignas(16) float stage[128][33];          // combined Dt chunk (32 j) per (i,b) row
+  alignas(16) float stage[128][TJ + 1];      // drained Dt tile (fp32 values), row = (i,b)
   alignas(16) uint8_t perm[R][TJ];           // per (row, 32-chunk): local j sorted by code
   alignas(16) float scale[TJ];               // s_j of the current j-tile (fp32)
-  alignas(16) uint8_t off[R][4][NLEV + 1];   // segment offsets per (row, chunk, level)
-  alignas(8) uint64_t full[MAX_STAGES], empty[MAX_STAGES], tfull, tempty;
+  alignas(16) uint8_t off[R][NCH][NLEV + 1]; // segment offsets per (row, chunk, level)
+  alignas(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   uint32_t tmem_slot;
 };
+
+__host__ __device__ inline int ktiles_of(int jt) { return (jt * TJ + TJ - 1) / TK + 1; }
 
 template <int NLEV>
 __global__ void __launch_bounds__(THREADS, 1)
 tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ Q,
-                const double* __restrict__ scale, int64_t m, int64_t n, int64_t P, int jsplit,
-                double* __restrict__ Cg) {
+                const double* __restrict__ scale, int64_t m, int64_t n, int64_t P,
+                const int4 jsplit, double* __restrict__ Cg) {
   constexpr int R = 128 / NLEV;
-  constexpr int STAGES = kStages<NLEV>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   TcSmem<NLEV>& sm = *reinterpret_cast<TcSmem<NLEV>*>(tiles + STAGES * STAGE_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r0 = (int64_t)(blockIdx.x >> 1) * R;
+  const int64_t r0 = (int64_t)(blockIdx.x / SPLIT) * R;
   const int NT = (int)((n + TJ - 1) / TJ);
-  // Two CTAs per row group: j-tiles [0, jsplit) and [jsplit, NT) (balanced triangle work);
-  // each writes its own partial C (summed in fixed order by the solve kernel).
-  const int half = blockIdx.x & 1;
-  const int jt_lo = half ? jsplit : 0, jt_hi = half ? NT : jsplit;
-  double* Cpart = Cg + (size_t)half * (size_t)m * NLEV * NLEV;
+  const int part = blockIdx.x % SPLIT;
+  const int bnd[SPLIT + 1] = {0, jsplit.x, jsplit.y, jsplit.z, NT};
+  const int jt_lo = bnd[part], jt_hi = bnd[part + 1];
+  double* Cpart = Cg + (size_t)part * (size_t)m * NLEV * NLEV;
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);
@@ -88,14 +107,14 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     if (lane == 0) {
       uint32_t ks = 0;
       for (int jt = jt_lo; jt < jt_hi; ++jt)
-        for (int kt = 0; kt <= jt; ++kt, ++ks) {
+        for (int kt = 0; kt < ktiles_of(jt); ++kt, ++ks) {
           const uint32_t s = ks % STAGES;
           mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
           uint8_t* st = tiles + s * STAGE_BYTES;
-          mbar_arrive_expect_tx(&sm.full[s], 3 * TILE_BYTES);
+          mbar_arrive_expect_tx(&sm.full[s], 3 * B_TILE);
 #pragma unroll
           for (int l = 0; l < 3; ++l)
-            tma_load_2d(st + (1 + l) * TILE_BYTES, &tmap, &sm.full[s], kt * TK, (int)(l * P + jt * TJ));
+            tma_load_2d(st + A_TILE + l * B_TILE, &tmap, &sm.full[s], kt * TK, (int)(l * P + jt * TJ));
         }
     }
   } else if (warp == 1) {
@@ -105,20 +124,18 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       for (int jt = jt_lo; jt < jt_hi; ++jt) {
         mbar_wait(&sm.tempty, ((jt - jt_lo) & 1) ^ 1);
         tc_fence_after();
-        for (int kt = 0; kt <= jt; ++kt, ++ks) {
+        for (int kt = 0; kt < ktiles_of(jt); ++kt, ++ks) {
           const uint32_t s = ks % STAGES;
           mbar_wait(&sm.full[s], (ks / STAGES) & 1);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(tiles + s * STAGE_BYTES);
 #pragma unroll
           for (int l = 0; l < 3; ++l) {
-            const uint32_t b_addr = a_addr + (1 + l) * TILE_BYTES;
+            const uint32_t b_addr = a_addr + A_TILE + l * B_TILE;
 #pragma unroll
-            for (int kk = 0; kk < TK / 32; ++kk) {
-              const uint64_t ad = umma_desc_sw128(a_addr + kk * 32, 16, 1024);
-              const uint64_t bd = umma_desc_sw128(b_addr + kk * 32, 16, 1024);
-              mma_i8(tmem + l * TJ, ad, bd, IDESC, (kt > 0 || kk > 0) ? 1u : 0u);
-            }
+            for (int kk = 0; kk < TK / 32; ++kk)
+              mma_i8(tmem + l * TJ, umma_desc_sw64(a_addr + kk * 32), umma_desc_sw64(b_addr + kk * 32),
+                     IDESC, (kt > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&sm.empty[s]);
         }
@@ -126,19 +143,22 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       }
     }
   } else if (warp < 4) {
-    // ---------------- one-hot producers: A[(i,b)][k] = [q_ik == b] (int8), K-major SW128.
+    // ---------------- one-hot producers: A[(i,b)][k] = [q_ik == b] (int8), K-major SW64.
     // Thread pt owns (row i, 16-column chunk c) pairs and writes the NLEV one-hot rows of
-    // each; its 16 code bytes are loaded one k-tile ahead (no shared staging, no barriers).
+    // each; its 16 code bytes are loaded one stage ahead.
     const int pt = threadIdx.x - 64;  // 0..63
-    constexpr int PAIRS = R * (TK / 16) / NPROD;  // (i, c) pairs per thread = 16 / NLEV
-    auto load_codes = [&](int kt, uint4 (&v)[PAIRS]) {
+    constexpr int CPR = TK / 16;                 // 16-byte chunks per row (4)
+    constexpr int PAIRS = R * CPR / NPROD;       // (i, c) pairs per thread = 8 / NLEV (>= 1 for NLEV <= 8)
+    constexpr int NP = PAIRS > 0 ? PAIRS : 1;
+    // NLEV = 16: R * CPR = 32 pairs < 64 threads -> threads pt >= 32 idle in the code loads
+    auto load_codes = [&](int kt, uint4 (&v)[NP]) {
 #pragma unroll
-      for (int u = 0; u < PAIRS; ++u) {
+      for (int u = 0; u < NP; ++u) {
         const int pr = pt + NPROD * u;
-        const int i = pr / (TK / 16), c = pr % (TK / 16);
+        const int i = pr / CPR, c = pr % CPR;
         const int64_t row = r0 + i, k = (int64_t)kt * TK + c * 16;
         v[u] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (row < m) {
+        if (i < R && row < m) {
           const uint8_t* src = Q + row * n + k;
           if (k + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
             v[u] = __ldg(reinterpret_cast<const uint4*>(src));
@@ -150,23 +170,48 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         }
       }
     };
-    uint4 cur[PAIRS], nxt[PAIRS];
+    // levels handled per thread: NLEV = 16 splits each pair's 16 levels over two threads
+    constexpr int LSPLIT = (R * CPR < NPROD) ? NPROD / (R * CPR) : 1;  // 2 for NLEV = 16
+    constexpr int LPT = NLEV / LSPLIT;                                 // levels per thread
+    const int pid = (LSPLIT > 1) ? (pt % (R * CPR)) : pt;
+    const int lbase = (LSPLIT > 1) ? (pt / (R * CPR)) * LPT : 0;
+    uint4 cur[NP], nxt[NP];
+    auto load_mine = [&](int kt, uint4 (&v)[NP]) {
+      if constexpr (LSPLIT > 1) {
+        const int i = pid / CPR, c = pid % CPR;
+        const int64_t row = r0 + i, k = (int64_t)kt * TK + c * 16;
+        v[0] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        if (row < m) {
+          const uint8_t* src = Q + row * n + k;
+          if (k + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            v[0] = __ldg(reinterpret_cast<const uint4*>(src));
+          } else {
+            uint8_t* vb = reinterpret_cast<uint8_t*>(&v[0]);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) vb[q] = (k + q < n) ? src[q] : (uint8_t)0xFF;
+          }
+        }
+      } else {
+        load_codes(kt, v);
+      }
+    };
     int jt = jt_lo, kt = 0;
-    if (jt < jt_hi) load_codes(kt, cur);
+    if (jt < jt_hi) load_mine(kt, cur);
     uint32_t ks = 0;
     while (jt < jt_hi) {
       const uint32_t s = ks % STAGES;
       int jn = jt, kn = kt + 1;
-      if (kn > jn) { ++jn; kn = 0; }
-      if (jn < jt_hi) load_codes(kn, nxt);  // prefetch the next k-tile's codes
+      if (kn >= ktiles_of(jn)) { ++jn; kn = 0; }
+      if (jn < jt_hi) load_mine(kn, nxt);  // prefetch the next stage's codes
       mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
       uint8_t* A = tiles + s * STAGE_BYTES;
 #pragma unroll
-      for (int u = 0; u < PAIRS; ++u) {
-        const int pr = pt + NPROD * u;
-        const int i = pr / (TK / 16), c = pr % (TK / 16);
+      for (int u = 0; u < NP; ++u) {
+        const int pr = (LSPLIT > 1) ? pid : pt + NPROD * u;
+        const int i = pr / CPR, c = pr % CPR;
 #pragma unroll
-        for (int b = 0; b < NLEV; ++b) {
+        for (int bl = 0; bl < LPT; ++bl) {
+          const int b = lbase + bl;
           const int rr = i * NLEV + b;
           const uint32_t bb = 0x01010101u * (uint32_t)b;
           uint4 o;
@@ -174,33 +219,44 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           o.y = __vcmpeq4(cur[u].y, bb) & 0x01010101u;
           o.z = __vcmpeq4(cur[u].z, bb) & 0x01010101u;
           o.w = __vcmpeq4(cur[u].w, bb) & 0x01010101u;
-          *reinterpret_cast<uint4*>(A + rr * 128 + ((c ^ (rr & 7)) << 4)) = o;
+          // SW64: 16-byte chunk c of 64-byte row rr sits at chunk c ^ ((rr >> 1) & 3)
+          *reinterpret_cast<uint4*>(A + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4)) = o;
         }
       }
       fence_proxy_async_smem();
       mbar_arrive(&sm.full[s]);
 #pragma unroll
-      for (int u = 0; u < PAIRS; ++u) cur[u] = nxt[u];
+      for (int u = 0; u < NP; ++u) cur[u] = nxt[u];
       jt = jn;
       kt = kn;
       ++ks;
     }
   } else {
-    // ---------------- epilogue: exact integer sums -> fp32 values -> sorted segmented walk
+    // ---------------- epilogue
     const int et = threadIdx.x - 128;      // 0..127 == TMEM lane == (i, b)
     const int quarter = warp & 3;          // == et / 32
     const int i = et / NLEV, b = et % NLEV;
-    (void)b;
     double acc[NLEV];
 #pragma unroll
     for (int a = 0; a < NLEV; ++a) acc[a] = 0.0;
     for (int jt = jt_lo; jt < jt_hi; ++jt) {
       const int64_t J0 = (int64_t)jt * TJ;
-      // sorted order of each row's 32-column chunks of this j-tile (counting sort by code)
-      for (int task = quarter; task < R * 4; task += 4) {
-        const int ri = task >> 2, c = task & 3;
+      // (1) sorted order of each row's 32-column chunks (counting sort by code); overlaps MMA
+      constexpr int NTASK = (R * NCH + 3) / 4;
+      int codes[NTASK];
+#pragma unroll
+      for (int u = 0; u < NTASK; ++u) {
+        const int task = quarter + 4 * u;
+        const int ri = task / NCH, c = task % NCH;
         const int64_t row = r0 + ri, j = J0 + c * 32 + lane;
-        const int code = (row < m && j < n) ? (int)Q[row * n + j] : 0xFF;
+        codes[u] = (task < R * NCH && row < m && j < n) ? (int)__ldg(Q + row * n + j) : 0xFF;
+      }
+#pragma unroll
+      for (int u = 0; u < NTASK; ++u) {
+        const int task = quarter + 4 * u;
+        if (task >= R * NCH) break;
+        const int ri = task / NCH, c = task % NCH;
+        const int code = codes[u];
         const unsigned lt = (1u << lane) - 1u;
         int base = 0, pos = -1;
 #pragma unroll
@@ -215,38 +271,39 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       }
       if (et < TJ) sm.scale[et] = (J0 + et < n) ? (float)scale[J0 + et] : 0.0f;
       named_bar_sync(1, 128);
+      // (2) drain: exact int32 digit sums -> fp32 (* s_j) into the staging tile, release TMEM
       mbar_wait(&sm.tfull, (jt - jt_lo) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t d0[32], d1[32], d2[32];
-        const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + c * 32;
-        tmem_ld32(tb, d0);
-        tmem_ld32(tb + TJ, d1);
-        tmem_ld32(tb + 2 * TJ, d2);
+      for (int g = 0; g < TJ / 16; ++g) {
+        uint32_t d0[16], d1[16], d2[16];
+        const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + g * 16;
+        tmem_ld16(tb, d0);
+        tmem_ld16(tb + TJ, d1);
+        tmem_ld16(tb + 2 * TJ, d2);
         tmem_ld_wait();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          // exact int32 digit sums -> fp32 value (one rounding per step, ~2^-24 relative)
+        for (int t = 0; t < 16; ++t) {
           const float v = fmaf((float)(int)d0[t], 65536.0f,
                                fmaf((float)(int)d1[t], 256.0f, (float)(int)d2[t]));
-          sm.stage[et][t] = v * sm.scale[c * 32 + t];
+          sm.stage[et][g * 16 + t] = v * sm.scale[g * 16 + t];
         }
-        __syncwarp();
-        // only this thread's own stage row is read below: no CTA-wide barrier needed
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.tempty);  // the next j-tile's MMAs may start now
+      // (3) sorted segmented walk over this thread's own staging row
+#pragma unroll 1
+      for (int c = 0; c < NCH; ++c) {
 #pragma unroll
         for (int a = 0; a < NLEV; ++a) {
           const int s0 = sm.off[i][c][a], s1 = sm.off[i][c][a + 1];
           float s = 0.0f;
-          for (int q = s0; q < s1; ++q) s += sm.stage[et][sm.perm[i][c * 32 + q]];
+          for (int q = s0; q < s1; ++q) s += sm.stage[et][c * 32 + sm.perm[i][c * 32 + q]];
           acc[a] += (double)s;
         }
-        __syncwarp();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tempty);
-      named_bar_sync(1, 128);  // perm/off/scale are rewritten for the next j-tile
+      named_bar_sync(1, 128);  // perm/off/scale/stage are rewritten for the next j-tile
     }
     const int64_t row = r0 + i;
     if (row < m) {
@@ -317,27 +374,33 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   CUtensorMap tmap;
   cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)(3 * P)};
   cuuint64_t strides[1] = {(cuuint64_t)P};
-  cuuint32_t box[2] = {TK, TJ};
+  cuuint32_t box[2] = {TK, TJ};  // 64 k (bytes) x 128 j
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)Hq, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error(GANQ_ERR_CUDA, "tgram: cuTensorMapEncodeTiled failed (%d)", (int)r);
     return GANQ_ERR_CUDA;
   }
   constexpr int R = 128 / NLEV;
-  const size_t smem = 1024 + kStages<NLEV> * STAGE_BYTES + sizeof(TcSmem<NLEV>);
+  const size_t smem = 1024 + STAGES * STAGE_BYTES + sizeof(TcSmem<NLEV>);
   GANQ_CUDA_TRY(cudaFuncSetAttribute(tgram_tc_kernel<NLEV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-  // split the triangle of j-tiles (work of tile jt ~ jt + 1) into two halves of equal work
+  // split the j-tiles (work of tile jt = ktiles_of(jt)) into SPLIT ranges of equal work
   const int NT = (int)((n + TJ - 1) / TJ);
-  const int64_t total = (int64_t)NT * (NT + 1) / 2;
-  int jsplit = 0;
+  int64_t total = 0;
+  for (int jt = 0; jt < NT; ++jt) total += ktiles_of(jt);
+  int bnd[SPLIT - 1];
   int64_t acc = 0;
-  while (jsplit < NT && 2 * (acc + jsplit + 1) <= total) acc += ++jsplit;
+  int jt = 0;
+  for (int p = 1; p < SPLIT; ++p) {
+    while (jt < NT && SPLIT * (acc + ktiles_of(jt)) <= p * total) acc += ktiles_of(jt++);
+    bnd[p - 1] = jt;
+  }
+  const int4 jsplit = make_int4(bnd[0], bnd[1], bnd[2], 0);
   const unsigned groups = (unsigned)((m + R - 1) / R);
-  tgram_tc_kernel<NLEV><<<2 * groups, THREADS, smem, st>>>(tmap, Q, scale, m, n, P, jsplit, Cg);
+  tgram_tc_kernel<NLEV><<<SPLIT * groups, THREADS, smem, st>>>(tmap, Q, scale, m, n, P, jsplit, Cg);
   GANQ_LAUNCH_CHECK("tgram_tc_kernel");
   return GANQ_OK;
 }

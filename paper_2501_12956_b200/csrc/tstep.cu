@@ -16,6 +16,8 @@
 namespace ganq {
 namespace {
 
+constexpr int kTgramSplit = 4;  // == SPLIT in tgram_tc.cu
+
 // Per row (one warp): D_i[a] = sum_j [q_ij=a] H_jj, b_i[a] = sum_j [q_ij=a] (W H)_ij and the
 // level counts (fp64 accumulation; lanes over j, warp-shuffle reduction in fixed order).
 template <int NLEV>
@@ -75,13 +77,16 @@ tsolve_kernel(double* __restrict__ G, const double* __restrict__ Dv, const doubl
   const bool used = cnt[row * NLEV + l] > 0;
   double g[NLEV];
   double maxdiag = 0.0;
-  // assemble G = C + C^T + D; C (strict lower sums j > k) arrives as two partials
-  // (j-tile halves, tgram_tc.cu) in G[0..m) and G[m..2m), added in fixed order
-  const double* G2 = G + (size_t)m * NLEV * NLEV;
+  // assemble G = C + C^T + D; C (strict lower sums j > k) arrives as GANQ_TGRAM_SPLIT
+  // partials (j-tile ranges, tgram_tc.cu) stacked along m, added in fixed order
+  const size_t pstride = (size_t)m * NLEV * NLEV;
 #pragma unroll
   for (int c = 0; c < NLEV; ++c) {
-    const double clc = G[(row * NLEV + l) * NLEV + c] + G2[(row * NLEV + l) * NLEV + c];
-    const double ccl = G[(row * NLEV + c) * NLEV + l] + G2[(row * NLEV + c) * NLEV + l];
+    double clc = 0.0, ccl = 0.0;
+    for (int p = 0; p < kTgramSplit; ++p) {
+      clc += G[p * pstride + (row * NLEV + l) * NLEV + c];
+      ccl += G[p * pstride + (row * NLEV + c) * NLEV + l];
+    }
     g[c] = clc + ccl + (c == l ? Dv[row * NLEV + l] : 0.0);
   }
   __syncwarp();
