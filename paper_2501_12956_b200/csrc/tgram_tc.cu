@@ -23,6 +23,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 
 #include "ganq_internal.cuh"
@@ -58,7 +60,7 @@ template <int NLEV>
 struct TcSmem {
   static constexpr int R = 128 / NLEV;
   alignas(16) float stage[128][TJ + 1];      // drained Dt tile (fp32 values), row = (i,b)
-  alignas(16) uint8_t perm[R][TJ];           // per (row, 32-chunk): local j sorted by code
+  alignas(16) uint8_t ipos[R][TJ];           // per (row, 32-chunk): sorted position of each j
   alignas(16) float scale[TJ];               // s_j of the current j-tile (fp32)
   alignas(16) uint8_t off[R][NCH][NLEV + 1]; // segment offsets per (row, chunk, level)
   alignas(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
@@ -71,7 +73,7 @@ template <int NLEV>
 __global__ void __launch_bounds__(THREADS, 1)
 tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ Q,
                 const double* __restrict__ scale, int64_t m, int64_t n, int64_t P,
-                const int4 jsplit, double* __restrict__ Cg) {
+                const int4 jsplit, double* __restrict__ Cg, int dbg) {
   constexpr int R = 128 / NLEV;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -144,81 +146,72 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     }
   } else if (warp < 4) {
     // ---------------- one-hot producers: A[(i,b)][k] = [q_ik == b] (int8), K-major SW64.
-    // Thread pt owns (row i, 16-column chunk c) pairs and writes the NLEV one-hot rows of
-    // each; its 16 code bytes are loaded one stage ahead.
+    // 8 passes per stage; in each pass thread pt writes one 16-byte chunk c of one one-hot row
+    // (i, b), lanes ordered so that a warp stores 512 contiguous bytes (no bank conflicts).
+    // Each lane loads NSLOT of the stage's R*4 code chunks (one stage ahead); a pass gets its
+    // chunk by shuffles (the source slot is a compile-time function of the pass).
     const int pt = threadIdx.x - 64;  // 0..63
-    constexpr int CPR = TK / 16;                 // 16-byte chunks per row (4)
-    constexpr int PAIRS = R * CPR / NPROD;       // (i, c) pairs per thread = 8 / NLEV (>= 1 for NLEV <= 8)
-    constexpr int NP = PAIRS > 0 ? PAIRS : 1;
-    // NLEV = 16: R * CPR = 32 pairs < 64 threads -> threads pt >= 32 idle in the code loads
-    auto load_codes = [&](int kt, uint4 (&v)[NP]) {
+    constexpr int CPR = TK / 16;                // 16-byte chunks per 64-byte row (4)
+    constexpr int IPR = NLEV * CPR;             // (b, c) items per row i
+    constexpr int RP = NPROD / IPR;             // rows per pass (1 for NLEV = 16)
+    constexpr int PASSES = R / RP;              // 8
+    constexpr int NSLOT = R * CPR / 32;         // code chunks loaded per lane (1, 2, 4, 8)
+    const int ri = pt / IPR, item = pt % IPR, b = item / CPR, c = item % CPR;
+    const uint32_t bb = 0x01010101u * (uint32_t)b;
+    auto load_codes = [&](int kt, uint4 (&v)[NSLOT]) {
 #pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        const int pr = pt + NPROD * u;
-        const int i = pr / CPR, c = pr % CPR;
-        const int64_t row = r0 + i, k = (int64_t)kt * TK + c * 16;
-        v[u] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (i < R && row < m) {
-          const uint8_t* src = Q + row * n + k;
-          if (k + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            v[u] = __ldg(reinterpret_cast<const uint4*>(src));
-          } else {
-            uint8_t* vb = reinterpret_cast<uint8_t*>(&v[u]);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) vb[q] = (k + q < n) ? src[q] : (uint8_t)0xFF;
-          }
-        }
-      }
-    };
-    // levels handled per thread: NLEV = 16 splits each pair's 16 levels over two threads
-    constexpr int LSPLIT = (R * CPR < NPROD) ? NPROD / (R * CPR) : 1;  // 2 for NLEV = 16
-    constexpr int LPT = NLEV / LSPLIT;                                 // levels per thread
-    const int pid = (LSPLIT > 1) ? (pt % (R * CPR)) : pt;
-    const int lbase = (LSPLIT > 1) ? (pt / (R * CPR)) * LPT : 0;
-    uint4 cur[NP], nxt[NP];
-    auto load_mine = [&](int kt, uint4 (&v)[NP]) {
-      if constexpr (LSPLIT > 1) {
-        const int i = pid / CPR, c = pid % CPR;
-        const int64_t row = r0 + i, k = (int64_t)kt * TK + c * 16;
-        v[0] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      for (int sl = 0; sl < NSLOT; ++sl) {
+        const int idx = sl * 32 + lane;         // chunk (i, cc) = (idx / CPR, idx % CPR)
+        const int i = idx / CPR, cc = idx % CPR;
+        const int64_t row = r0 + i, k = (int64_t)kt * TK + cc * 16;
+        v[sl] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
         if (row < m) {
           const uint8_t* src = Q + row * n + k;
           if (k + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            v[0] = __ldg(reinterpret_cast<const uint4*>(src));
+            v[sl] = __ldg(reinterpret_cast<const uint4*>(src));
           } else {
-            uint8_t* vb = reinterpret_cast<uint8_t*>(&v[0]);
+            uint8_t* vb = reinterpret_cast<uint8_t*>(&v[sl]);
 #pragma unroll
             for (int q = 0; q < 16; ++q) vb[q] = (k + q < n) ? src[q] : (uint8_t)0xFF;
           }
         }
-      } else {
-        load_codes(kt, v);
       }
     };
+    // byte-wise (x == b) -> 0x01 / 0x00 for codes < 16 or 0xFF: no borrow crosses a byte
+    auto onehot = [&](uint32_t x) {
+      const uint32_t y = (x ^ bb) | 0x80808080u;
+      return (~(y - 0x01010101u) & 0x80808080u) >> 7;
+    };
+    uint4 cur[NSLOT], nxt[NSLOT];
     int jt = jt_lo, kt = 0;
-    if (jt < jt_hi) load_mine(kt, cur);
+    if (jt < jt_hi) load_codes(kt, cur);
     uint32_t ks = 0;
     while (jt < jt_hi) {
       const uint32_t s = ks % STAGES;
       int jn = jt, kn = kt + 1;
       if (kn >= ktiles_of(jn)) { ++jn; kn = 0; }
-      if (jn < jt_hi) load_mine(kn, nxt);  // prefetch the next stage's codes
+      if (jn < jt_hi) load_codes(kn, nxt);  // prefetch the next stage's codes
       mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
       uint8_t* A = tiles + s * STAGE_BYTES;
 #pragma unroll
-      for (int u = 0; u < NP; ++u) {
-        const int pr = (LSPLIT > 1) ? pid : pt + NPROD * u;
-        const int i = pr / CPR, c = pr % CPR;
-#pragma unroll
-        for (int bl = 0; bl < LPT; ++bl) {
-          const int b = lbase + bl;
+      for (int ps = 0; ps < PASSES; ++ps) {
+        const int i = ps * RP + ri;
+        const int idx = i * CPR + c;
+        const int src = idx & 31;
+        // slot of chunk idx: (ps*RP*CPR + ri*CPR + c) / 32 == (ps*RP*CPR) / 32 (static)
+        const int sl = (ps * RP * CPR) / 32;
+        uint4 w;
+        w.x = __shfl_sync(0xffffffffu, cur[sl].x, src);
+        w.y = __shfl_sync(0xffffffffu, cur[sl].y, src);
+        w.z = __shfl_sync(0xffffffffu, cur[sl].z, src);
+        w.w = __shfl_sync(0xffffffffu, cur[sl].w, src);
+        if (!(dbg & 2)) {
           const int rr = i * NLEV + b;
-          const uint32_t bb = 0x01010101u * (uint32_t)b;
           uint4 o;
-          o.x = __vcmpeq4(cur[u].x, bb) & 0x01010101u;
-          o.y = __vcmpeq4(cur[u].y, bb) & 0x01010101u;
-          o.z = __vcmpeq4(cur[u].z, bb) & 0x01010101u;
-          o.w = __vcmpeq4(cur[u].w, bb) & 0x01010101u;
+          o.x = onehot(w.x);
+          o.y = onehot(w.y);
+          o.z = onehot(w.z);
+          o.w = onehot(w.w);
           // SW64: 16-byte chunk c of 64-byte row rr sits at chunk c ^ ((rr >> 1) & 3)
           *reinterpret_cast<uint4*>(A + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4)) = o;
         }
@@ -226,7 +219,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       fence_proxy_async_smem();
       mbar_arrive(&sm.full[s]);
 #pragma unroll
-      for (int u = 0; u < NP; ++u) cur[u] = nxt[u];
+      for (int sl = 0; sl < NSLOT; ++sl) cur[sl] = nxt[sl];
       jt = jn;
       kt = kn;
       ++ks;
@@ -267,7 +260,8 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           base += __popc(bal);
         }
         if (lane == 0) sm.off[ri][c][NLEV] = (uint8_t)base;
-        if (pos >= 0) sm.perm[ri][c * 32 + pos] = (uint8_t)lane;
+        // invalid columns (j >= n, rows >= m) go after every segment
+        sm.ipos[ri][c * 32 + lane] = (uint8_t)(pos >= 0 ? pos : 31);
       }
       if (et < TJ) sm.scale[et] = (J0 + et < n) ? (float)scale[J0 + et] : 0.0f;
       named_bar_sync(1, 128);
@@ -286,21 +280,35 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         for (int t = 0; t < 16; ++t) {
           const float v = fmaf((float)(int)d0[t], 65536.0f,
                                fmaf((float)(int)d1[t], 256.0f, (float)(int)d2[t]));
-          sm.stage[et][g * 16 + t] = v * sm.scale[g * 16 + t];
+          const int x = g * 16 + t;  // write in sorted order within its 32-column chunk
+          sm.stage[et][(x & ~31) + sm.ipos[i][x]] = v * sm.scale[x];
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.tempty);  // the next j-tile's MMAs may start now
-      // (3) sorted segmented walk over this thread's own staging row
+      // (3) segment sums over this thread's own (sorted) staging row: prefix sums in place,
+      //     segment a of chunk c = P[off[a+1]] - P[off[a]]
 #pragma unroll 1
-      for (int c = 0; c < NCH; ++c) {
+      for (int c = 0; c < ((dbg & 1) ? 0 : NCH); ++c) {
+        float* row = &sm.stage[et][c * 32];
+        float v[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = row[q];
+        float p = 0.0f;
+        row[0] = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 31; ++q) {
+          p += v[q];
+          row[q + 1] = p;  // P[q + 1]; P[32] is never needed (segments end <= 31 < 32?)
+        }
+        const float ptot = p + v[31];
 #pragma unroll
         for (int a = 0; a < NLEV; ++a) {
           const int s0 = sm.off[i][c][a], s1 = sm.off[i][c][a + 1];
-          float s = 0.0f;
-          for (int q = s0; q < s1; ++q) s += sm.stage[et][c * 32 + sm.perm[i][c * 32 + q]];
-          acc[a] += (double)s;
+          const float hi = (s1 == 32) ? ptot : row[s1];
+          const float lo = row[s0];  // s0 <= 31
+          acc[a] += (s1 > s0) ? (double)(hi - lo) : 0.0;
         }
       }
       named_bar_sync(1, 128);  // perm/off/scale/stage are rewritten for the next j-tile
@@ -400,7 +408,8 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   }
   const int4 jsplit = make_int4(bnd[0], bnd[1], bnd[2], 0);
   const unsigned groups = (unsigned)((m + R - 1) / R);
-  tgram_tc_kernel<NLEV><<<SPLIT * groups, THREADS, smem, st>>>(tmap, Q, scale, m, n, P, jsplit, Cg);
+  static const int dbg = getenv("GANQ_TGRAM_DBG") ? atoi(getenv("GANQ_TGRAM_DBG")) : 0;
+  tgram_tc_kernel<NLEV><<<SPLIT * groups, THREADS, smem, st>>>(tmap, Q, scale, m, n, P, jsplit, Cg, dbg);
   GANQ_LAUNCH_CHECK("tgram_tc_kernel");
   return GANQ_OK;
 }
