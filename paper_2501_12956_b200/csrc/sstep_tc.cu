@@ -18,7 +18,7 @@
 // the 128 sequential decisions per panel with the in-panel feedback in fp32 FMA.
 //
 // Warps: 0 = TMA producer, 1 = MMA issuer (+TMEM owner), 2-5 = TMEM readers (one lane
-// quarter each), 6 = panel (decisions).
+// quarter each), 6-9 = panel group (4 lanes per row).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -34,16 +34,19 @@ constexpr int PW = 128;             // panel width (UMMA M)
 constexpr int UB = 32;              // u per block (128 B of fp32: one swizzle row)
 constexpr int STAGES = 3;
 constexpr int NBUF = 8;             // TMEM accumulator buffers (32 columns each)
+constexpr int CS = 4;               // cluster size: row groups sharing each LhatT tile (multicast)
+constexpr uint16_t CMASK = (1u << CS) - 1u;
 constexpr int A_BYTES = PW * UB * 4;   // 16 KB
 constexpr int B_BYTES = RB * UB * 4;   // 4 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int THREADS = 224;
+constexpr int THREADS = 320;   // 10 warps: TMA, MMA, 4 readers, 4 panel
 constexpr uint32_t IDESC = umma_idesc(/*tf32*/ 2, 0, 0, PW, RB);
 
 struct SsSmem {
   alignas(128) float Ld[PW][PW];         // Lhat[jb + c][jb + c2] of the current panel (TMA)
   alignas(16) float As[2][PW][RB + 1];   // drained feedback per (panel column, row), 2 buffers
   alignas(16) float es[32][RB + 1];      // residuals of the current sub-panel (column, row)
+  alignas(16) uint8_t cs[32][RB + 4];    // codes of the current sub-panel (column, row)
   alignas(8) uint64_t full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF];
   alignas(8) uint64_t acc_ready[2], as_free[2], ebar, ldbar;
   uint32_t tmem_slot;
@@ -105,7 +108,8 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLhi, const __grid_constant
     prefetch_tmap(&tmEhi);
     prefetch_tmap(&tmElo);
     prefetch_tmap(&tmLd);
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], 1); }
+    // empty[s] collects one (multicast) MMA commit from every CTA of the cluster
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CS); }
     for (int b = 0; b < NBUF; ++b) { mbar_init(&sm.tfull[b], 1); mbar_init(&sm.tempty[b], 4); }
     for (int b = 0; b < 2; ++b) { mbar_init(&sm.acc_ready[b], 4); mbar_init(&sm.as_free[b], 1); }
     mbar_init(&sm.ebar, 1);
@@ -115,8 +119,10 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLhi, const __grid_constant
   if (warp == 1) tmem_alloc(&sm.tmem_slot, NBUF * RB);
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // every CTA's barriers exist before any multicast targets them
   tc_fence_after();
   const uint32_t tmem = sm.tmem_slot;
+  const uint32_t crank = cluster_ctarank();
 
   if (warp == 0) {
     // ---------------- TMA producer: blocks of target q = 1..P-1, source panels oldest first
@@ -140,8 +146,10 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLhi, const __grid_constant
             mbar_wait(&sm.empty[s], ((kb / STAGES) & 1) ^ 1);
             uint8_t* st = tiles + s * STAGE_BYTES;
             mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
-            tma_load_2d(st, &tmLhi, &sm.full[s], u0, jb);
-            tma_load_2d(st + A_BYTES, &tmLlo, &sm.full[s], u0, jb);
+            // this CTA's quarter of the LhatT hi/lo tiles, multicast to the whole cluster
+            const int sl = (int)crank * (PW / CS);
+            tma_load_2d_mc(st + sl * 128, &tmLhi, &sm.full[s], u0, jb + sl, CMASK);
+            tma_load_2d_mc(st + A_BYTES + sl * 128, &tmLlo, &sm.full[s], u0, jb + sl, CMASK);
             tma_load_2d(st + 2 * A_BYTES, &tmEhi, &sm.full[s], u0, (int)r0);
             tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tmElo, &sm.full[s], u0, (int)r0);
           }
@@ -175,7 +183,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLhi, const __grid_constant
                 mma_tf32(d, ad, bd, IDESC, (pass > 0 || kk > 0) ? 1u : 0u);
               }
             }
-            mma_commit(&sm.empty[s]);
+            mma_commit_mc(&sm.empty[s], CMASK);  // frees stage s in every CTA of the cluster
             mma_commit(&sm.tfull[buf]);
           }
     }
@@ -209,82 +217,172 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLhi, const __grid_constant
       if (lane == 0) mbar_arrive(&sm.acc_ready[ab]);
     }
   } else {
-    // ---------------- panel warp: lane = row, sequential decisions
-    const int64_t row = r0 + lane;
+    // ---------------- panel group (warps 6-9): 4 lanes per row, sequential decisions.
+    // Lane (r, sub) holds levels [4 sub, 4 sub + 4) of row r's codebook and the accumulators
+    // of the sub-panel columns c = 4 k + sub.  Per column: the owner lane's z and w are
+    // broadcast, each lane takes the argmin over its 4 levels, two shuffle rounds combine the
+    // candidates (distance, then index: the first index wins ties exactly as in a sequential
+    // strict '<' scan), and every lane forms e = w - t_q and updates its own accumulators.
+    constexpr int LPL = NLEV / 4 > 0 ? NLEV / 4 : 1;   // levels per lane
+    const int pl = threadIdx.x - 192;                  // 0..127
+    const int rr = pl >> 2, sub = pl & 3;              // row within CTA, quarter
+    const int64_t row = r0 + rr;
     const bool live = row < m;
-    float t[NLEV];
+    const unsigned gmask = 0xffffffffu;
+    const int gbase = lane & ~3;                       // first lane of this row's group
+    float t[LPL];
 #pragma unroll
-    for (int s = 0; s < NLEV; ++s) t[s] = live ? T[row * NLEV + s] : 0.0f;
+    for (int x = 0; x < LPL; ++x) {
+      const int lev = sub * LPL + x;
+      t[x] = (live && lev < NLEV) ? T[row * NLEV + lev] : 0.0f;
+    }
     const float* wrow = W + (live ? row : 0) * n;
+    const int64_t off = np - n;                        // right-aligned storage offset
+    const uint32_t pbar = 3;                           // named barrier of the panel group
     for (int q = 0; q < P; ++q) {
       const int64_t jb = n - (int64_t)PW * (q + 1);
       const int ab = q & 1;
       mbar_wait(&sm.acc_ready[ab], (q >> 1) & 1);
       mbar_wait(&sm.ldbar, q & 1);
+      float wn[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t j = jb + 32 * (PW / 32 - 1) + 4 * k + sub;
+        wn[k] = (j >= 0) ? wrow[j] : 0.0f;
+      }
 #pragma unroll 1
       for (int sp = PW / 32 - 1; sp >= 0; --sp) {
         const int64_t j0 = jb + 32 * sp;     // first column of the sub-panel (may be < 0)
-        float a[32], w[32];
-        uint8_t code[32];
+        float a[8], w[8];
 #pragma unroll
-        for (int x = 0; x < 32; ++x) {
-          a[x] = sm.As[ab][32 * sp + x][lane];
-          w[x] = (j0 + x >= 0) ? wrow[j0 + x] : 0.0f;
+        for (int k = 0; k < 8; ++k) {
+          a[k] = sm.As[ab][32 * sp + 4 * k + sub][rr];
+          w[k] = wn[k];
+        }
+        if (sp > 0) {  // prefetch the next sub-panel's weights
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int64_t j = j0 - 32 + 4 * k + sub;
+            wn[k] = (j >= 0) ? wrow[j] : 0.0f;
+          }
         }
 #pragma unroll
         for (int cc = 31; cc >= 0; --cc) {
-          const float z = __fadd_rn(w[cc], a[cc]);
-          int qv;
-          float tq;
-          argmin_tree<NLEV>(z, t, qv, tq);
+          const int own = cc & 3, kc = cc >> 2;
+          const float zl = __fadd_rn(w[kc], a[kc]);                       // valid on the owner
+          const float z = __shfl_sync(gmask, zl, gbase | own);
+          const float wc = __shfl_sync(gmask, w[kc], gbase | own);
+          // local argmin over this lane's levels (first index on ties)
+          float bd = fabsf(__fsub_rn(z, t[0]));
+          int bi = sub * LPL;
+          float bt = t[0];
+#pragma unroll
+          for (int x = 1; x < LPL; ++x) {
+            const float d = fabsf(__fsub_rn(z, t[x]));
+            const bool better = d < bd;
+            bd = better ? d : bd;
+            bi = better ? sub * LPL + x : bi;
+            bt = better ? t[x] : bt;
+          }
+          if (NLEV < 4 && sub * LPL >= NLEV) bd = __int_as_float(0x7f800000);  // no levels here
+#pragma unroll
+          for (int o = 1; o < 4; o <<= 1) {
+            const float od = __shfl_xor_sync(gmask, bd, o);
+            const int oi = __shfl_xor_sync(gmask, bi, o);
+            const float ot = __shfl_xor_sync(gmask, bt, o);
+            const bool take = (od < bd) || (od == bd && oi < bi);
+            bd = take ? od : bd;
+            bi = take ? oi : bi;
+            bt = take ? ot : bt;
+          }
           const bool real = j0 + cc >= 0;
-          const float ec = real ? __fsub_rn(w[cc], tq) : 0.0f;
-          sm.es[cc][lane] = ec;
-          code[cc] = (uint8_t)qv;
-          const float* lrow = &sm.Ld[32 * sp + cc][32 * sp];  // Lhat[j][j0 + c2] (0 if OOB)
+          const float ec = real ? __fsub_rn(wc, bt) : 0.0f;
+          if (sub == own) {
+            sm.es[cc][rr] = ec;
+            sm.cs[cc][rr] = (uint8_t)bi;
+          }
+          const float* lrow = &sm.Ld[32 * sp + cc][32 * sp + sub];  // Lhat[j][j0 + 4 k + sub]
 #pragma unroll
-          for (int c2 = 0; c2 < cc; ++c2) a[c2] = fmaf(ec, lrow[c2], a[c2]);
+          for (int k = 0; k < 8; ++k)
+            if (4 * k + sub < cc) a[k] = fmaf(ec, lrow[4 * k], a[k]);
         }
+        named_bar_sync(pbar, 128);  // es / cs of this sub-panel complete
+        // stores: lane sub writes columns [8 sub, 8 sub + 8) of its row
         if (live) {
+          float ev[8];
+          uint8_t cv[8];
 #pragma unroll
-          for (int x = 0; x < 32; ++x) {
-            const int64_t j = j0 + x;
-            if (j >= 0) {
-              Q[row * n + j] = code[x];
-              const float ex = sm.es[x][lane];
-              const float hi = tf32_rna(ex);
-              Ehi[row * np + (np - n) + j] = hi;
-              Elo[row * np + (np - n) + j] = __fsub_rn(ex, hi);
+          for (int x = 0; x < 8; ++x) {
+            ev[x] = sm.es[8 * sub + x][rr];
+            cv[x] = sm.cs[8 * sub + x][rr];
+          }
+          const int64_t jj = j0 + 8 * sub;
+          if (jj >= 0) {
+            float* eh = Ehi + row * np + off + jj;
+            float* el = Elo + row * np + off + jj;
+            float hi[8], lo[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+              hi[x] = tf32_rna(ev[x]);
+              lo[x] = __fsub_rn(ev[x], hi[x]);
+            }
+            // storage column off + jj is a multiple of 4 (right-aligned pitch): 16-byte stores
+            reinterpret_cast<float4*>(eh)[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            reinterpret_cast<float4*>(eh)[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+            reinterpret_cast<float4*>(el)[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            reinterpret_cast<float4*>(el)[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
+            uint8_t* qd = Q + row * n + jj;
+            if ((reinterpret_cast<uintptr_t>(qd) & 7) == 0) {
+              uint2 pk;
+              pk.x = cv[0] | (cv[1] << 8) | (cv[2] << 16) | ((uint32_t)cv[3] << 24);
+              pk.y = cv[4] | (cv[5] << 8) | (cv[6] << 16) | ((uint32_t)cv[7] << 24);
+              *reinterpret_cast<uint2*>(qd) = pk;
+            } else {
+#pragma unroll
+              for (int x = 0; x < 8; ++x) qd[x] = cv[x];
+            }
+          } else {
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+              const int64_t j = jj + x;
+              if (j >= 0) {
+                const float hi = tf32_rna(ev[x]);
+                Ehi[row * np + off + j] = hi;
+                Elo[row * np + off + j] = __fsub_rn(ev[x], hi);
+                Q[row * n + j] = cv[x];
+              }
             }
           }
         }
-        // feedback of this sub-panel into the sub-panels left of it (same panel)
+        // feedback of this sub-panel into the sub-panels left of it: lane sub owns target
+        // columns [8 sub, 8 sub + 8) of every earlier sub-panel
 #pragma unroll 1
         for (int tp = 0; tp < sp; ++tp) {
-          float ac[32];
+          float ac[8];
 #pragma unroll
-          for (int x = 0; x < 32; ++x) ac[x] = sm.As[ab][32 * tp + x][lane];
-#pragma unroll 2
+          for (int x = 0; x < 8; ++x) ac[x] = sm.As[ab][32 * tp + 8 * sub + x][rr];
+#pragma unroll 4
           for (int cc = 0; cc < 32; ++cc) {
-            const float ec = sm.es[cc][lane];
-            const float4* lrow = reinterpret_cast<const float4*>(&sm.Ld[32 * sp + cc][32 * tp]);
-#pragma unroll
-            for (int x4 = 0; x4 < 8; ++x4) {
-              const float4 l = lrow[x4];
-              ac[4 * x4 + 0] = fmaf(ec, l.x, ac[4 * x4 + 0]);
-              ac[4 * x4 + 1] = fmaf(ec, l.y, ac[4 * x4 + 1]);
-              ac[4 * x4 + 2] = fmaf(ec, l.z, ac[4 * x4 + 2]);
-              ac[4 * x4 + 3] = fmaf(ec, l.w, ac[4 * x4 + 3]);
-            }
+            const float ec = sm.es[cc][rr];
+            const float4* lrow = reinterpret_cast<const float4*>(&sm.Ld[32 * sp + cc][32 * tp + 8 * sub]);
+            const float4 l0 = lrow[0], l1 = lrow[1];
+            ac[0] = fmaf(ec, l0.x, ac[0]);
+            ac[1] = fmaf(ec, l0.y, ac[1]);
+            ac[2] = fmaf(ec, l0.z, ac[2]);
+            ac[3] = fmaf(ec, l0.w, ac[3]);
+            ac[4] = fmaf(ec, l1.x, ac[4]);
+            ac[5] = fmaf(ec, l1.y, ac[5]);
+            ac[6] = fmaf(ec, l1.z, ac[6]);
+            ac[7] = fmaf(ec, l1.w, ac[7]);
           }
 #pragma unroll
-          for (int x = 0; x < 32; ++x) sm.As[ab][32 * tp + x][lane] = ac[x];
+          for (int x = 0; x < 8; ++x) sm.As[ab][32 * tp + 8 * sub + x][rr] = ac[x];
         }
-        __syncwarp();
+        named_bar_sync(pbar, 128);  // As updated, es / cs free for the next sub-panel
       }
       fence_proxy_async_global();  // residual stores -> visible to the TMA (async proxy)
-      __syncwarp();
-      if (lane == 0) {
+      named_bar_sync(pbar, 128);
+      if (pl == 0) {
         mbar_arrive(&sm.ebar);
         mbar_arrive(&sm.as_free[ab]);
       }
@@ -292,6 +390,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLhi, const __grid_constant
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, NBUF * RB);
 }
@@ -371,7 +470,7 @@ ganq_status_t launch_t(const float* W, const float* Lhat, const float* LThi, con
   CUtensorMap mLhi, mLlo, mEhi, mElo, mLd;
   // inner extent = the padded pitch np (>= 4 elements: TMA needs >= 16 bytes per row); the
   // padding columns are zero (LhatT, Lhat) or never inside a box (E: u-blocks end below n)
-  if (!make_map(&mLhi, LThi, np, n, np, UB, PW) || !make_map(&mLlo, LTlo, np, n, np, UB, PW) ||
+  if (!make_map(&mLhi, LThi, np, n, np, UB, PW / CS) || !make_map(&mLlo, LTlo, np, n, np, UB, PW / CS) ||
       !make_map(&mEhi, Ehi, np, m, np, UB, RB) || !make_map(&mElo, Elo, np, m, np, UB, RB) ||
       !make_map(&mLd, Lhat, np, n, np, PW, PW, /*swizzle*/ false)) {
     set_error(GANQ_ERR_CUDA, "sstep: tensor map encoding failed");
@@ -380,8 +479,21 @@ ganq_status_t launch_t(const float* W, const float* Lhat, const float* LThi, con
   const size_t smem = 1024 + STAGES * STAGE_BYTES + sizeof(SsSmem);
   GANQ_CUDA_TRY(cudaFuncSetAttribute(sstep_tc_kernel<NLEV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-  sstep_tc_kernel<NLEV><<<(unsigned)((m + RB - 1) / RB), THREADS, smem, st>>>(
-      mLhi, mLlo, mEhi, mElo, mLd, W, T, m, n, np, Q, Ehi, Elo);
+  const unsigned groups = (unsigned)((m + RB - 1) / RB);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((groups + CS - 1) / CS * CS);  // whole clusters; extra CTAs own no rows
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GANQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, sstep_tc_kernel<NLEV>, mLhi, mLlo, mEhi, mElo, mLd, W, T, m, n,
+                                   np, Q, Ehi, Elo));
   GANQ_LAUNCH_CHECK("sstep_tc_kernel");
   return GANQ_OK;
 }
