@@ -69,14 +69,20 @@ __global__ void precondition_kernel(const double* __restrict__ H, int64_t n, int
 }
 
 // ---------------------------------------------------------------- diagonal block
+// One CTA of 256 threads = 16 x 16; thread (tx, ty) owns the 4 x 4 elements
+// (ty + 16 a, tx + 16 b) of the 64 x 64 block (no integer division in the loops).
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A, int64_t n, int64_t k0,
                                                          int* __restrict__ status) {
   __shared__ double s[NB * LDS];
   const int kb = (int)min((int64_t)NB, n - k0);
-  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
-    const int r = idx / kb, c = idx % kb;
-    s[r * LDS + c] = (c <= r) ? A[(k0 + r) * n + k0 + c] : 0.0;
-  }
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = ty + 16 * a, c = tx + 16 * b;
+      s[r * LDS + c] = (r < kb && c <= r) ? A[(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
+    }
   __syncthreads();
   for (int c = 0; c < kb; ++c) {
     double piv = s[c * LDS + c];
@@ -84,24 +90,36 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A,
       if (threadIdx.x == 0) atomicMin(status, (int)(k0 + c));
       piv = 1.0;
     }
-    const double lcc = sqrt(piv);
+    const double inv = 1.0 / sqrt(piv);
+    __syncthreads();  // everyone has read the pivot
+    // scale column c below the diagonal; the diagonal becomes sqrt(piv)
+    if (threadIdx.x < NB) {
+      const int r = threadIdx.x;
+      if (r > c) s[r * LDS + c] *= inv;
+      if (r == c) s[r * LDS + c] = piv * inv;
+    }
     __syncthreads();
-    // column c below the diagonal
-    for (int r = c + 1 + threadIdx.x; r < kb; r += blockDim.x) s[r * LDS + c] /= lcc;
-    if (threadIdx.x == 0) s[c * LDS + c] = lcc;
-    __syncthreads();
-    // trailing rank-1 update of the lower part
-    const int m = kb - c - 1;
-    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-      const int r = c + 1 + idx / m, q = c + 1 + idx % m;
-      if (q <= r) s[r * LDS + q] -= s[r * LDS + c] * s[q * LDS + c];
+    // trailing rank-1 update of the lower part (rows, cols > c)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int r = ty + 16 * a;
+      if (r <= c) continue;
+      const double lrc = s[r * LDS + c];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int q = tx + 16 * b;
+        if (q > c && q <= r) s[r * LDS + q] -= lrc * s[q * LDS + c];
+      }
     }
     __syncthreads();
   }
-  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
-    const int r = idx / kb, c = idx % kb;
-    if (c <= r) A[(k0 + r) * n + k0 + c] = s[r * LDS + c];
-  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = ty + 16 * a, c = tx + 16 * b;
+      if (r < kb && c <= r) A[(k0 + r) * n + k0 + c] = s[r * LDS + c];
+    }
 }
 
 // ---------------------------------------------------------------- panel TRSM
@@ -109,9 +127,9 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A,
 __global__ void __launch_bounds__(256) trsm_panel_kernel(double* __restrict__ A, int64_t n, int64_t k0) {
   __shared__ double s[NB * LDS];
   const int kb = (int)min((int64_t)NB, n - k0);
-  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
-    const int r = idx / kb, c = idx % kb;
-    s[r * LDS + c] = (c <= r) ? A[(k0 + r) * n + k0 + c] : 0.0;
+  for (int r = threadIdx.x >> 6; r < kb; r += 4) {
+    const int c = threadIdx.x & 63;
+    if (c < kb) s[r * LDS + c] = (c <= r) ? A[(k0 + r) * n + k0 + c] : 0.0;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -143,8 +161,8 @@ __global__ void __launch_bounds__(256) syrk_trailing_kernel(double* __restrict__
   double* Pj = syrk_smem + NB * LDS;
   const int64_t base = k0 + NB;  // first trailing row/col (only called when k0 + NB < n)
   const int64_t i0 = base + (int64_t)ti * NB, j0 = base + (int64_t)tj * NB;
-  for (int idx = threadIdx.x; idx < NB * NB; idx += blockDim.x) {
-    const int r = idx / NB, c = idx % NB;
+  for (int r = threadIdx.x >> 6; r < NB; r += 4) {
+    const int c = threadIdx.x & 63;
     Pi[r * LDS + c] = (i0 + r < n) ? A[(i0 + r) * n + k0 + c] : 0.0;
     Pj[r * LDS + c] = (j0 + r < n) ? A[(j0 + r) * n + k0 + c] : 0.0;
   }

@@ -14,11 +14,12 @@
 //
 // Pipeline (one CTA per (row group, j range); SPLIT CTAs per group over balanced j ranges):
 //   warp 0     TMA: the three digit tiles of H (128 j x 64 k, SWIZZLE_64B) per stage
-//   warp 1     MMA issuer (+TMEM owner): 3 int32 accumulators of 128 columns
-//   warps 2-3  one-hot producers: A[(i,b)][k] = [q_ik == b] in the K-major SW64 layout,
-//              codes prefetched one stage ahead
-//   warps 4-7  epilogue: drain TMEM (digits -> fp32 * s_j) into a shared staging tile and
-//              release the accumulators at once, then the sorted walk overlaps the next
+//   warp 1     MMA issuer (+TMEM owner): 3 int32 accumulators of 128 columns, A from TMEM
+//   warps 2-5  one-hot producers, one per TMEM lane quarter: lane (i,b) builds its 64 bytes
+//              [q_ik == b] per stage in registers and tcgen05.st's them into a TMEM ring
+//              (no shared-memory traffic for A; codes prefetched one stage ahead)
+//   warps 6-9  epilogue: drain TMEM (digits -> fp32 * s_j) into a shared staging tile and
+//              release the accumulators at once, then the segment sums overlap the next
 //              j-tile's MMAs
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -34,13 +35,13 @@ namespace {
 
 constexpr int TJ = 128;          // j per tile (UMMA N)
 constexpr int TK = 64;           // k per stage (64-byte swizzle rows of int8)
-constexpr int STAGES = 4;
-constexpr int A_TILE = 128 * TK;                 // 8 KB one-hot operand
+constexpr int STAGES = 6;
 constexpr int B_TILE = TJ * TK;                  // 8 KB digit tile of H
-constexpr int STAGE_BYTES = A_TILE + 3 * B_TILE; // 32 KB
+constexpr int STAGE_BYTES = 3 * B_TILE;          // 24 KB (the one-hot A operand lives in TMEM)
 constexpr int SPLIT = 4;                         // CTAs per row group (balanced j ranges)
-constexpr int THREADS = 256;
-constexpr int NPROD = 64;                        // one-hot producer threads (warps 2-3)
+constexpr int THREADS = 320;                     // 10 warps
+constexpr int A_COL0 = 3 * TJ;                   // TMEM: 3 accumulators, then the A ring
+constexpr int A_COLS = TK / 4;                   // 16 columns of 4 int8 per stage
 constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile (sorting unit)
 constexpr uint32_t IDESC = umma_idesc_s8(128, TJ);
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
@@ -91,7 +92,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&sm.full[s], 1 + NPROD);
+      mbar_init(&sm.full[s], 1 + 4);  // TMA bytes + one arrive per producer warp
       mbar_init(&sm.empty[s], 1);
     }
     mbar_init(&sm.tfull, 1);
@@ -116,7 +117,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           mbar_arrive_expect_tx(&sm.full[s], 3 * B_TILE);
 #pragma unroll
           for (int l = 0; l < 3; ++l)
-            tma_load_2d(st + A_TILE + l * B_TILE, &tmap, &sm.full[s], kt * TK, (int)(l * P + jt * TJ));
+            tma_load_2d(st + l * B_TILE, &tmap, &sm.full[s], kt * TK, (int)(l * P + jt * TJ));
         }
     }
   } else if (warp == 1) {
@@ -130,47 +131,39 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           const uint32_t s = ks % STAGES;
           mbar_wait(&sm.full[s], (ks / STAGES) & 1);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(tiles + s * STAGE_BYTES);
+          const uint32_t s_addr = smem_u32(tiles + s * STAGE_BYTES);
+          const uint32_t a_tmem = tmem + A_COL0 + s * A_COLS;
 #pragma unroll
           for (int l = 0; l < 3; ++l) {
-            const uint32_t b_addr = a_addr + A_TILE + l * B_TILE;
+            const uint32_t b_addr = s_addr + l * B_TILE;
 #pragma unroll
             for (int kk = 0; kk < TK / 32; ++kk)
-              mma_i8(tmem + l * TJ, umma_desc_sw64(a_addr + kk * 32), umma_desc_sw64(b_addr + kk * 32),
-                     IDESC, (kt > 0 || kk > 0) ? 1u : 0u);
+              mma_i8_ts(tmem + l * TJ, a_tmem + kk * 8, umma_desc_sw64(b_addr + kk * 32), IDESC,
+                        (kt > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&sm.empty[s]);
         }
         mma_commit(&sm.tfull);
       }
     }
-  } else if (warp < 4) {
-    // ---------------- one-hot producers: A[(i,b)][k] = [q_ik == b] (int8), K-major SW64.
-    // 8 passes per stage; in each pass thread pt writes one 16-byte chunk c of one one-hot row
-    // (i, b), lanes ordered so that a warp stores 512 contiguous bytes (no bank conflicts).
-    // Each lane loads NSLOT of the stage's R*4 code chunks (one stage ahead); a pass gets its
-    // chunk by shuffles (the source slot is a compile-time function of the pass).
-    const int pt = threadIdx.x - 64;  // 0..63
-    constexpr int CPR = TK / 16;                // 16-byte chunks per 64-byte row (4)
-    constexpr int IPR = NLEV * CPR;             // (b, c) items per row i
-    constexpr int RP = NPROD / IPR;             // rows per pass (1 for NLEV = 16)
-    constexpr int PASSES = R / RP;              // 8
-    constexpr int NSLOT = R * CPR / 32;         // code chunks loaded per lane (1, 2, 4, 8)
-    const int ri = pt / IPR, item = pt % IPR, b = item / CPR, c = item % CPR;
+  } else if (warp < 6) {
+    // ---------------- one-hot producers: TMEM lane (i, b) <- [q_ik == b] for the stage's 64 k
+    const int pl = (warp & 3) * 32 + lane;  // == TMEM lane (this warp's quarter)
+    const int i = pl / NLEV, b = pl % NLEV;
+    const int64_t row = r0 + i;
     const uint32_t bb = 0x01010101u * (uint32_t)b;
-    auto load_codes = [&](int kt, uint4 (&v)[NSLOT]) {
+    const uint8_t* qrow = Q + (row < m ? row : 0) * n;
+    auto load_codes = [&](int kt, uint4 (&v)[TK / 16]) {
 #pragma unroll
-      for (int sl = 0; sl < NSLOT; ++sl) {
-        const int idx = sl * 32 + lane;         // chunk (i, cc) = (idx / CPR, idx % CPR)
-        const int i = idx / CPR, cc = idx % CPR;
-        const int64_t row = r0 + i, k = (int64_t)kt * TK + cc * 16;
-        v[sl] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      for (int c = 0; c < TK / 16; ++c) {
+        const int64_t k = (int64_t)kt * TK + c * 16;
+        v[c] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
         if (row < m) {
-          const uint8_t* src = Q + row * n + k;
+          const uint8_t* src = qrow + k;
           if (k + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            v[sl] = __ldg(reinterpret_cast<const uint4*>(src));
+            v[c] = __ldg(reinterpret_cast<const uint4*>(src));
           } else {
-            uint8_t* vb = reinterpret_cast<uint8_t*>(&v[sl]);
+            uint8_t* vb = reinterpret_cast<uint8_t*>(&v[c]);
 #pragma unroll
             for (int q = 0; q < 16; ++q) vb[q] = (k + q < n) ? src[q] : (uint8_t)0xFF;
           }
@@ -182,7 +175,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       const uint32_t y = (x ^ bb) | 0x80808080u;
       return (~(y - 0x01010101u) & 0x80808080u) >> 7;
     };
-    uint4 cur[NSLOT], nxt[NSLOT];
+    uint4 cur[TK / 16], nxt[TK / 16];
     int jt = jt_lo, kt = 0;
     if (jt < jt_hi) load_codes(kt, cur);
     uint32_t ks = 0;
@@ -191,43 +184,31 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       int jn = jt, kn = kt + 1;
       if (kn >= ktiles_of(jn)) { ++jn; kn = 0; }
       if (jn < jt_hi) load_codes(kn, nxt);  // prefetch the next stage's codes
-      mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
-      uint8_t* A = tiles + s * STAGE_BYTES;
+      uint32_t v[16];
 #pragma unroll
-      for (int ps = 0; ps < PASSES; ++ps) {
-        const int i = ps * RP + ri;
-        const int idx = i * CPR + c;
-        const int src = idx & 31;
-        // slot of chunk idx: (ps*RP*CPR + ri*CPR + c) / 32 == (ps*RP*CPR) / 32 (static)
-        const int sl = (ps * RP * CPR) / 32;
-        uint4 w;
-        w.x = __shfl_sync(0xffffffffu, cur[sl].x, src);
-        w.y = __shfl_sync(0xffffffffu, cur[sl].y, src);
-        w.z = __shfl_sync(0xffffffffu, cur[sl].z, src);
-        w.w = __shfl_sync(0xffffffffu, cur[sl].w, src);
-        if (!(dbg & 2)) {
-          const int rr = i * NLEV + b;
-          uint4 o;
-          o.x = onehot(w.x);
-          o.y = onehot(w.y);
-          o.z = onehot(w.z);
-          o.w = onehot(w.w);
-          // SW64: 16-byte chunk c of 64-byte row rr sits at chunk c ^ ((rr >> 1) & 3)
-          *reinterpret_cast<uint4*>(A + rr * 64 + ((c ^ ((rr >> 1) & 3)) << 4)) = o;
-        }
+      for (int c = 0; c < TK / 16; ++c) {
+        v[4 * c + 0] = onehot(cur[c].x);
+        v[4 * c + 1] = onehot(cur[c].y);
+        v[4 * c + 2] = onehot(cur[c].z);
+        v[4 * c + 3] = onehot(cur[c].w);
       }
-      fence_proxy_async_smem();
-      mbar_arrive(&sm.full[s]);
+      mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
+      tc_fence_after();
+      tmem_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS, v);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.full[s]);
 #pragma unroll
-      for (int sl = 0; sl < NSLOT; ++sl) cur[sl] = nxt[sl];
+      for (int c = 0; c < TK / 16; ++c) cur[c] = nxt[c];
       jt = jn;
       kt = kn;
       ++ks;
     }
   } else {
     // ---------------- epilogue
-    const int et = threadIdx.x - 128;      // 0..127 == TMEM lane == (i, b)
-    const int quarter = warp & 3;          // == et / 32
+    const int quarter = warp & 3;          // TMEM lane quarter of this warp
+    const int et = quarter * 32 + lane;    // 0..127 == TMEM lane == (i, b)
     const int i = et / NLEV, b = et % NLEV;
     double acc[NLEV];
 #pragma unroll
