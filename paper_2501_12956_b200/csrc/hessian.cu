@@ -8,12 +8,14 @@
 //
 // Tiling: one CTA owns a 128 (i) x 256 (j) output tile that touches the lower
 // triangle and loops over all token chunks of GANQ_HESSIAN_CHUNK tokens.  A
-// chunk accumulates in fp32 in TMEM (bf16 products are exact in fp32); the
-// epilogue adds it into the fp64 H in chunk order (reading R-12).  TMEM holds
-// two 256-column accumulators so the epilogue of chunk c overlaps the MMAs of
-// chunk c+1.  Warp roles: 0 = TMA producer, 1 = MMA issuer (+TMEM owner),
-// 2..5 = epilogue (one TMEM lane quarter each).  A final kernel mirrors the
-// strict lower triangle onto the upper one, so H is exactly symmetric.
+// chunk accumulates in fp32 in TMEM columns [0, 256) (bf16 products are exact in
+// fp32; the tensor-core adds truncate, so chains are kept to one chunk).  The
+// epilogue folds each chunk into a round-to-nearest fp32 running sum kept in TMEM
+// columns [256, 512) (tcgen05.ld + add + tcgen05.st) and writes the tile to the
+// fp64 H once, at the end (reading R-12): no per-chunk read-modify-write of H.
+// Warp roles: 0 = TMA producer, 1 = MMA issuer (+TMEM owner), 2..5 = epilogue
+// (one TMEM lane quarter each).  A final kernel mirrors the strict lower triangle
+// onto the upper one, so H is exactly symmetric.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -95,11 +97,10 @@ hessian_syrk_kernel(const __grid_constant__ CUtensorMap tmap, int64_t p, int64_t
     if (lane == 0) {
       uint32_t kb = 0;
       for (int64_t c = 0; c < nchunks; ++c) {
-        const uint32_t buf = (uint32_t)(c & 1);
-        const uint32_t use = (uint32_t)(c >> 1);
-        mbar_wait(&tempty[buf], (use & 1) ^ 1);
+        const uint32_t buf = 0;
+        mbar_wait(&tempty[0], ((uint32_t)c & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + buf * BN;
+        const uint32_t d_tmem = tmem_base;
         const int64_t t0 = c * GANQ_HESSIAN_CHUNK;
         const int64_t t1 = min(p, t0 + GANQ_HESSIAN_CHUNK);
         bool first = true;
@@ -120,39 +121,53 @@ hessian_syrk_kernel(const __grid_constant__ CUtensorMap tmap, int64_t p, int64_t
           mma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
         }
         mma_commit(&tfull[buf]);  // chunk accumulator ready for the epilogue
+        (void)buf;
       }
     }
   } else {
-    // ---------------- epilogue: TMEM -> registers -> fp64 H (chunk order)
+    // ---------------- epilogue: fold chunks into the TMEM fp32 running sum, write H once
     const int quarter = warp & 3;  // TMEM lanes [32*quarter, +32) are accessible to this warp
     const int row = quarter * 32 + lane;
     const int64_t gi = (int64_t)i0 + row;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
     for (int64_t c = 0; c < nchunks; ++c) {
-      const uint32_t buf = (uint32_t)(c & 1);
-      const uint32_t use = (uint32_t)(c >> 1);
-      mbar_wait(&tfull[buf], use & 1);
+      mbar_wait(&tfull[0], (uint32_t)c & 1);
       tc_fence_after();
-      const bool store = (c == 0) && !accumulate;
 #pragma unroll 1
       for (int cg = 0; cg < BN / 16; ++cg) {
-        uint32_t v[16];
-        tmem_ld16(tmem_base + ((uint32_t)(quarter * 32) << 16) + buf * BN + cg * 16, v);
+        uint32_t v[16], r[16];
+        tmem_ld16(lane_base + cg * 16, v);
+        if (c > 0) tmem_ld16(lane_base + BN + cg * 16, r);
         tmem_ld_wait();
-        if (gi < n) {
-          double* hrow = H + gi * n;
+        if (c > 0) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int64_t gj = (int64_t)j0 + cg * 16 + q;
-            if (gj < n && gj <= gi) {
-              const double val = (double)__uint_as_float(v[q]);
-              hrow[gj] = store ? val : hrow[gj] + val;
-            }
+          for (int q = 0; q < 16; ++q)
+            v[q] = __float_as_uint(__fadd_rn(__uint_as_float(r[q]), __uint_as_float(v[q])));
+        }
+        tmem_st16(lane_base + BN + cg * 16, v);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[0]);
+    }
+    tc_fence_after();
+#pragma unroll 1
+    for (int cg = 0; cg < BN / 16; ++cg) {
+      uint32_t v[16];
+      tmem_ld16(lane_base + BN + cg * 16, v);
+      tmem_ld_wait();
+      if (gi < n) {
+        double* hrow = H + gi * n;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int64_t gj = (int64_t)j0 + cg * 16 + q;
+          if (gj < n && gj <= gi) {
+            const double val = (double)__uint_as_float(v[q]);
+            hrow[gj] = accumulate ? hrow[gj] + val : val;
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
     }
   }
 
