@@ -79,8 +79,8 @@ struct StageScope {
 namespace {
 
 struct Layout {
-  size_t A64, Lhat, LThi, LTlo, Ehi, Elo, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, status, mean,
-      per_row, total_d, end;
+  size_t A64, Lhat, LThi, LTlo, Ehi, Elo, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, Xhi, Xlo, Hhi,
+      Hlo, status, mean, per_row, total_d, end;
 };
 
 Layout make_layout(int64_t m, int64_t n, int nlev) {
@@ -111,6 +111,11 @@ Layout make_layout(int64_t m, int64_t n, int nlev) {
   const size_t P = (size_t)tq_pitch(n);
   L.Hq = take(3 * P * P);
   L.qscale = take(P * sizeof(double));
+  const size_t kp = (size_t)gemm_pitch(n);
+  L.Xhi = take((size_t)m * kp * sizeof(float));  // tf32 split of W (then of E for the objective)
+  L.Xlo = take((size_t)m * kp * sizeof(float));
+  L.Hhi = take((size_t)n * kp * sizeof(float));  // tf32 split of H32
+  L.Hlo = take((size_t)n * kp * sizeof(float));
   L.status = take(sizeof(int));
   L.mean = take(sizeof(double));
   L.per_row = take((size_t)m * sizeof(double));
@@ -194,13 +199,15 @@ ganq_status_t factor(const double* H, int64_t n, const ganq_opts_t& o, void* ws,
 }
 
 // f = sum_i e_i H32 e_i^T with E, EH, per_row scratch; result left in ws.total_d (device).
-ganq_status_t objective_device(const float* W, const uint8_t* Q, const float* T, const float* H32,
-                               int64_t m, int64_t n, int nlev, float* E, float* EH, double* per_row,
-                               double* total, cudaStream_t st) {
+// Hhi/Hlo: the tf32 split of H32 (already computed); Xhi/Xlo: scratch for the split of E.
+ganq_status_t objective_device(const float* W, const uint8_t* Q, const float* T, const float* Hhi,
+                               const float* Hlo, int64_t m, int64_t n, int nlev, float* E, float* Xhi,
+                               float* Xlo, float* EH, double* per_row, double* total, cudaStream_t st) {
   ganq_status_t s;
   GANQ_STAGE(ST_OBJECTIVE);
   if ((s = launch_residual(W, Q, T, m, n, nlev, E, st))) return s;
-  if ((s = launch_gemm_f32(E, H32, EH, m, n, n, st))) return s;
+  if ((s = launch_split_tf32(E, m, n, Xhi, Xlo, st))) return s;
+  if ((s = launch_gemm_tf32x3(Xhi, Xlo, Hhi, Hlo, m, n, n, EH, st))) return s;
   if ((s = launch_rowdot(E, EH, m, n, per_row, st))) return s;
   return launch_sum(per_row, m, total, st);
 }
@@ -324,10 +331,15 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
     GANQ_STAGE(ST_DERIVE);
     if ((s = launch_tq_prep(H, n, at<int8_t>(ws, L.Hq), at<double>(ws, L.qscale), st))) return s;
   }
+  float* Hhi = at<float>(ws, L.Hhi);
+  float* Hlo = at<float>(ws, L.Hlo);
   {
-    // W H (fixed across iterations: W_i H S_i^T of Eq. 6)
+    // W H (fixed across iterations: W_i H S_i^T of Eq. 6), tf32x3 on the tensor cores
     GANQ_STAGE(ST_GEMM_WH);
-    if ((s = launch_gemm_f32(W, H32, WH, m, n, n, st))) return s;
+    if ((s = launch_split_tf32(H32, n, n, Hhi, Hlo, st))) return s;
+    if ((s = launch_split_tf32(W, m, n, at<float>(ws, L.Xhi), at<float>(ws, L.Xlo), st))) return s;
+    if ((s = launch_gemm_tf32x3(at<float>(ws, L.Xhi), at<float>(ws, L.Xlo), Hhi, Hlo, m, n, n, WH, st)))
+      return s;
   }
   {
     // T^0 (reading R-6)
@@ -356,8 +368,8 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
         return s;
     }
     if (o.obj_trace) {
-      if ((s = objective_device(W, Q, T, H32, m, n, nlev, E, EH, at<double>(ws, L.per_row),
-                                at<double>(ws, L.total_d), st)))
+      if ((s = objective_device(W, Q, T, Hhi, Hlo, m, n, nlev, E, at<float>(ws, L.Xhi), at<float>(ws, L.Xlo),
+                                EH, at<double>(ws, L.per_row), at<double>(ws, L.total_d), st)))
         return s;
       GANQ_CUDA_TRY(cudaMemcpyAsync(&o.obj_trace[k], at<double>(ws, L.total_d), sizeof(double),
                                     cudaMemcpyDeviceToHost, st));
@@ -370,12 +382,15 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
 
 size_t ganq_objective_workspace_size(int64_t m, int64_t n) {
   if (m < 1 || n < 1) return 0;
+  const size_t kp = (size_t)gemm_pitch(n);
   size_t off = 0;
   off = align_up(off + (size_t)n * n * sizeof(float), 256);      // H32
   off = align_up(off + (size_t)m * n * sizeof(float), 256);      // E
   off = align_up(off + (size_t)m * n * sizeof(float), 256);      // EH
   off = align_up(off + (size_t)m * sizeof(double), 256);         // per_row
   off = align_up(off + sizeof(double), 256);                     // total
+  off = align_up(off + 2 * (size_t)m * kp * sizeof(float), 256); // E hi / lo
+  off = align_up(off + 2 * (size_t)n * kp * sizeof(float), 256); // H hi / lo
   return off;
 }
 
@@ -408,11 +423,20 @@ ganq_status_t ganq_objective(const float* W, const uint8_t* Q, const float* T, c
   double* pr = at<double>(workspace, off);
   off = align_up(off + (size_t)m * sizeof(double), 256);
   double* tot = at<double>(workspace, off);
+  off = align_up(off + sizeof(double), 256);
+  const size_t kp = (size_t)gemm_pitch(n);
+  float* Xhi = at<float>(workspace, off);
+  float* Xlo = Xhi + (size_t)m * kp;
+  off = align_up(off + 2 * (size_t)m * kp * sizeof(float), 256);
+  float* Hhi = at<float>(workspace, off);
+  float* Hlo = Hhi + (size_t)n * kp;
   {
     GANQ_STAGE(ST_DERIVE);
     if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
+    if ((s = launch_split_tf32(H32, n, n, Hhi, Hlo, st))) return s;
   }
-  if ((s = objective_device(W, Q, T, H32, m, n, 1 << n_bits, E, EH, per_row ? per_row : pr, tot, st)))
+  if ((s = objective_device(W, Q, T, Hhi, Hlo, m, n, 1 << n_bits, E, Xhi, Xlo, EH, per_row ? per_row : pr,
+                            tot, st)))
     return s;
   GANQ_CUDA_TRY(cudaMemcpyAsync(out, tot, sizeof(double), cudaMemcpyDeviceToHost, st));
   GANQ_CUDA_TRY(cudaStreamSynchronize(st));
@@ -443,7 +467,11 @@ ganq_status_t ganq_tstep(const float* W, const uint8_t* Q, const double* H, int6
   if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
   if ((s = launch_tq_prep(H, n, at<int8_t>(workspace, L.Hq), at<double>(workspace, L.qscale), st)))
     return s;
-  if ((s = launch_gemm_f32(W, H32, WH, m, n, n, st))) return s;
+  if ((s = launch_split_tf32(H32, n, n, at<float>(workspace, L.Hhi), at<float>(workspace, L.Hlo), st))) return s;
+  if ((s = launch_split_tf32(W, m, n, at<float>(workspace, L.Xhi), at<float>(workspace, L.Xlo), st))) return s;
+  if ((s = launch_gemm_tf32x3(at<float>(workspace, L.Xhi), at<float>(workspace, L.Xlo), at<float>(workspace, L.Hhi),
+                              at<float>(workspace, L.Hlo), m, n, n, WH, st)))
+    return s;
   if (empty_level_rule == 1 && Tprev && Tprev != T)
     GANQ_CUDA_TRY(cudaMemcpyAsync(T, Tprev, sizeof(float) * (size_t)m * nlev, cudaMemcpyDeviceToDevice, st));
   GANQ_CUDA_TRY(cudaMemsetAsync(at<int>(workspace, L.fb), 0, sizeof(int) * (size_t)m, st));

@@ -58,9 +58,13 @@ ganq_status_t launch_lhat_split(const double* L, int64_t n, float* Lhat, float* 
 ganq_status_t launch_sstep_tc(const float* W, const float* Lhat, const float* LThi, const float* LTlo,
                               const float* T, int64_t m, int64_t n, int nlev, uint8_t* Q, float* Ehi,
                               float* Elo, cudaStream_t st);
+// gemm_tc.cu
+int64_t gemm_pitch(int64_t K);
+ganq_status_t launch_split_tf32(const float* X, int64_t rows, int64_t K, float* hi, float* lo,
+                                cudaStream_t st);
+ganq_status_t launch_gemm_tf32x3(const float* Ahi, const float* Alo, const float* Bhi, const float* Blo,
+                                 int64_t M, int64_t N, int64_t K, float* C, cudaStream_t st);
 // gemm.cu
-ganq_status_t launch_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N,
-                              int64_t K, cudaStream_t st);
 ganq_status_t launch_residual(const float* W, const uint8_t* Q, const float* T, int64_t m, int64_t n,
                               int nlev, float* E, cudaStream_t st);
 ganq_status_t launch_rowdot(const float* E, const float* EH, int64_t m, int64_t n, double* per_row,
