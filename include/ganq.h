@@ -152,7 +152,7 @@ ganq_status_t ganq_factor(const double* H, int64_t n, const ganq_opts_t* opts, d
  * launches[i] (kernel launches) for stage i < GANQ_PROFILE_STAGES; returns the stage count.
  * ganq_launch_count() is the total number of kernels this library launched (process-wide).
  */
-#define GANQ_PROFILE_STAGES 12
+#define GANQ_PROFILE_STAGES 13
 int ganq_profile_enable(int on);
 int ganq_profile_read(double* ms, int64_t* launches, int max_stages);
 const char* ganq_profile_stage_name(int stage);

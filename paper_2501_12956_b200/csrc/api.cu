@@ -35,11 +35,11 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 enum Stage {
   ST_HESSIAN = 0, ST_PRECOND, ST_CHOLESKY, ST_DERIVE, ST_GEMM_WH, ST_INIT, ST_SSTEP, ST_TGRAM,
-  ST_OBJECTIVE, ST_COPY, ST_TSTEP_ONLY, ST_FACTOR_COPY, ST_COUNT
+  ST_OBJECTIVE, ST_COPY, ST_TSTEP_ONLY, ST_FACTOR_COPY, ST_TSOLVE, ST_COUNT
 };
 static const char* kStageNames[ST_COUNT] = {
     "hessian", "precondition", "cholesky", "derive_operands", "gemm_wh", "init_codebook",
-    "sstep", "tstep", "objective", "copy", "tstep_api", "factor_copy"};
+    "sstep", "tgram", "objective", "copy", "tstep_api", "factor_copy", "tsolve"};
 static_assert(ST_COUNT == GANQ_PROFILE_STAGES, "stage table");
 
 struct Prof {
@@ -361,10 +361,16 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
     }
     {
       // T-update, raw H (reading R-4)
-      GANQ_STAGE(ST_TGRAM);
-      if ((s = launch_tstep(H, at<int8_t>(ws, L.Hq), at<double>(ws, L.qscale), WH, Q, m, n, nlev,
-                            o.empty_level_rule, T, at<double>(ws, L.G), at<double>(ws, L.Dv),
-                            at<double>(ws, L.b), at<int>(ws, L.cnt), at<int>(ws, L.fb), st)))
+      {
+        GANQ_STAGE(ST_TGRAM);
+        if ((s = launch_tgram_tc(at<int8_t>(ws, L.Hq), at<double>(ws, L.qscale), Q, m, n, nlev,
+                                 at<double>(ws, L.G), st)))
+          return s;
+      }
+      GANQ_STAGE(ST_TSOLVE);
+      if ((s = launch_tsolve(H, WH, Q, m, n, nlev, o.empty_level_rule, T, at<double>(ws, L.G),
+                             at<double>(ws, L.Dv), at<double>(ws, L.b), at<int>(ws, L.cnt), at<int>(ws, L.fb),
+                             st)))
         return s;
     }
     if (o.obj_trace) {
@@ -475,10 +481,12 @@ ganq_status_t ganq_tstep(const float* W, const uint8_t* Q, const double* H, int6
   if (empty_level_rule == 1 && Tprev && Tprev != T)
     GANQ_CUDA_TRY(cudaMemcpyAsync(T, Tprev, sizeof(float) * (size_t)m * nlev, cudaMemcpyDeviceToDevice, st));
   GANQ_CUDA_TRY(cudaMemsetAsync(at<int>(workspace, L.fb), 0, sizeof(int) * (size_t)m, st));
-  return launch_tstep(H, at<int8_t>(workspace, L.Hq), at<double>(workspace, L.qscale), WH, Q, m, n, nlev,
-                      empty_level_rule, T, at<double>(workspace, L.G), at<double>(workspace, L.Dv),
-                      at<double>(workspace, L.b), at<int>(workspace, L.cnt), at<int>(workspace, L.fb),
-                      st);
+  if ((s = launch_tgram_tc(at<int8_t>(workspace, L.Hq), at<double>(workspace, L.qscale), Q, m, n, nlev,
+                           at<double>(workspace, L.G), st)))
+    return s;
+  return launch_tsolve(H, WH, Q, m, n, nlev, empty_level_rule, T, at<double>(workspace, L.G),
+                       at<double>(workspace, L.Dv), at<double>(workspace, L.b), at<int>(workspace, L.cnt),
+                       at<int>(workspace, L.fb), st);
 }
 
 ganq_status_t ganq_factor(const double* H, int64_t n, const ganq_opts_t* opts, double* Lout,

@@ -43,9 +43,10 @@ ganq_status_t launch_derive_operands(const double* L, const double* H, int64_t n
 // tstep.cu
 ganq_status_t launch_init_codebook(const float* W, int64_t m, int64_t n, int nlev, float* T,
                                    cudaStream_t st);
-ganq_status_t launch_tstep(const double* H, const int8_t* Hq, const double* qscale, const float* WH,
-                           const uint8_t* Q, int64_t m, int64_t n, int nlev, int empty_rule, float* T,
-                           double* G, double* Dv, double* b, int* cnt, int* fallback, cudaStream_t st);
+// the T-update after the normal matrices (launch_tgram_tc): right-hand sides and the solves
+ganq_status_t launch_tsolve(const double* H, const float* WH, const uint8_t* Q, int64_t m, int64_t n, int nlev,
+                            int empty_rule, float* T, double* G, double* Dv, double* b, int* cnt, int* fallback,
+                            cudaStream_t st);
 // tgram_tc.cu
 int64_t tq_pitch(int64_t n);
 ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* scale, cudaStream_t st);
@@ -337,6 +338,10 @@ __host__ __device__ constexpr uint32_t umma_idesc(uint32_t ab_format, uint32_t a
 // kind::i8: signed int8 A and B (format 1), S32 accumulator (c_format 2), K-major operands.
 __host__ __device__ constexpr uint32_t umma_idesc_s8(uint32_t M, uint32_t N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+// kind::i8 with an unsigned (u8) A operand and a signed (s8) B operand, s32 accumulate
+__host__ __device__ constexpr uint32_t umma_idesc_u8s8(uint32_t M, uint32_t N) {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 #endif
 

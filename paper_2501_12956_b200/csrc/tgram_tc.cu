@@ -18,12 +18,13 @@
 //   warps 2-5  one-hot producers, one per TMEM lane quarter: lane (i,b) builds its 64 bytes
 //              [q_ik == b] per stage in registers and tcgen05.st's them into a TMEM ring
 //              (no shared-memory traffic for A; codes prefetched one stage ahead)
-//   warps 6-9  epilogue: drain TMEM (digits -> fp32 * s_j) into a shared staging tile and
-//              release the accumulators at once, then the segment sums overlap the next
-//              j-tile's MMAs
+//   warps 6-13 epilogue, two warps per lane quarter (one per column half): drain TMEM
+//              (digits -> fp32 * s_j) into a shared staging tile and release the accumulators
+//              at once, then the segment sums overlap the next j-tile's MMAs
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <mutex>
@@ -39,11 +40,14 @@ constexpr int STAGES = 6;
 constexpr int B_TILE = TJ * TK;                  // 8 KB digit tile of H
 constexpr int STAGE_BYTES = 3 * B_TILE;          // 24 KB (the one-hot A operand lives in TMEM)
 constexpr int SPLIT = 4;                         // CTAs per row group (balanced j ranges)
-constexpr int THREADS = 320;                     // 10 warps
+constexpr int CS = 2;                            // cluster: CS row groups share every H tile
+constexpr uint16_t CMASK = (1u << CS) - 1;
+constexpr int SLICE = TJ / CS;                   // j rows of each digit tile one CTA loads
+constexpr int THREADS = 448;                     // 14 warps
 constexpr int A_COL0 = 3 * TJ;                   // TMEM: 3 accumulators, then the A ring
 constexpr int A_COLS = TK / 4;                   // 16 columns of 4 int8 per stage
 constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile (sorting unit)
-constexpr uint32_t IDESC = umma_idesc_s8(128, TJ);
+constexpr uint32_t IDESC = umma_idesc_u8s8(128, TJ);  // A = one-hot bytes 0 / 128 (u8)
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
 
 // SW64 K-major UMMA descriptor: 64-byte rows, 8-row atoms of 512 B (SBO), layout type 4.
@@ -55,6 +59,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)4 << 61;
   return d;
+}
+
+// debug-only cycle accounting per warp role (GANQ_TGRAM_DBG & 16)
+__device__ unsigned long long g_tgprof[16];
+#define TP_T0(v) long long v = (dbg & 16) ? clock64() : 0
+#define TP_ACC(acc, v) do { if (dbg & 16) acc += clock64() - v; } while (0)
+__device__ __forceinline__ void tp_flush(int dbg, int lane, int slot, long long v) {
+  if ((dbg & 16) && lane == 0) atomicAdd(&g_tgprof[slot], (unsigned long long)v);
 }
 
 template <int NLEV>
@@ -69,12 +81,13 @@ struct TcSmem {
 };
 
 __host__ __device__ inline int ktiles_of(int jt) { return (jt * TJ + TJ - 1) / TK + 1; }
+static_assert(TJ == 2 * TK, "producers step ktiles_of by TJ / TK = 2");
 
 template <int NLEV>
 __global__ void __launch_bounds__(THREADS, 1)
 tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ Q,
                 const double* __restrict__ scale, int64_t m, int64_t n, int64_t P,
-                const int4 jsplit, double* __restrict__ Cg, int dbg) {
+                const int4 jsplit, int gp, double* __restrict__ Cg, int dbg) {
   constexpr int R = 128 / NLEV;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -82,9 +95,11 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   TcSmem<NLEV>& sm = *reinterpret_cast<TcSmem<NLEV>*>(tiles + STAGES * STAGE_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r0 = (int64_t)(blockIdx.x / SPLIT) * R;
+  // blockIdx.x = part * gp + group (gp = groups rounded up to whole clusters): the CS CTAs of a
+  // cluster hold consecutive row groups of the same j range and share each stage's H tiles
+  const int64_t r0 = (int64_t)(blockIdx.x % gp) * R;
   const int NT = (int)((n + TJ - 1) / TJ);
-  const int part = blockIdx.x % SPLIT;
+  const int part = blockIdx.x / gp;
   const int bnd[SPLIT + 1] = {0, jsplit.x, jsplit.y, jsplit.z, NT};
   const int jt_lo = bnd[part], jt_hi = bnd[part + 1];
   double* Cpart = Cg + (size_t)part * (size_t)m * NLEV * NLEV;
@@ -92,44 +107,62 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&sm.full[s], 1 + 4);  // TMA bytes + one arrive per producer warp
-      mbar_init(&sm.empty[s], 1);
+      mbar_init(&sm.full[s], 1 + 4);  // TMA bytes (all CS slices) + one arrive per producer warp
+      mbar_init(&sm.empty[s], CS);    // one (multicast) MMA commit from every CTA of the cluster
     }
     mbar_init(&sm.tfull, 1);
-    mbar_init(&sm.tempty, 4);
+    mbar_init(&sm.tempty, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(&sm.tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // every CTA's barriers exist before any multicast targets them
   tc_fence_after();
   const uint32_t tmem = sm.tmem_slot;
+  const uint32_t crank = cluster_ctarank();
 
   if (warp == 0) {
     // ---------------- TMA: three digit tiles of H per stage
     if (lane == 0) {
+      TP_T0(t_all);
+      long long w_empty = 0;
       uint32_t ks = 0;
       for (int jt = jt_lo; jt < jt_hi; ++jt)
         for (int kt = 0; kt < ktiles_of(jt); ++kt, ++ks) {
           const uint32_t s = ks % STAGES;
+          TP_T0(t0);
           mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
+          TP_ACC(w_empty, t0);
           uint8_t* st = tiles + s * STAGE_BYTES;
           mbar_arrive_expect_tx(&sm.full[s], 3 * B_TILE);
+          // this CTA's slice of j rows of each digit tile, multicast to the whole cluster
 #pragma unroll
           for (int l = 0; l < 3; ++l)
-            tma_load_2d(st + l * B_TILE, &tmap, &sm.full[s], kt * TK, (int)(l * P + jt * TJ));
+            tma_load_2d_mc(st + l * B_TILE + crank * SLICE * TK, &tmap, &sm.full[s], kt * TK,
+                           (int)(l * P + jt * TJ + crank * SLICE), CMASK);
         }
+      long long tot = 0;
+      TP_ACC(tot, t_all);
+      tp_flush(dbg, 0, 0, tot);
+      tp_flush(dbg, 0, 1, w_empty);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer
     if (lane == 0) {
+      TP_T0(t_all);
+      long long w_full = 0, w_tempty = 0;
       uint32_t ks = 0;
       for (int jt = jt_lo; jt < jt_hi; ++jt) {
+        TP_T0(t1);
         mbar_wait(&sm.tempty, ((jt - jt_lo) & 1) ^ 1);
+        TP_ACC(w_tempty, t1);
         tc_fence_after();
         for (int kt = 0; kt < ktiles_of(jt); ++kt, ++ks) {
           const uint32_t s = ks % STAGES;
+          TP_T0(t0);
           mbar_wait(&sm.full[s], (ks / STAGES) & 1);
+          TP_ACC(w_full, t0);
           tc_fence_after();
           const uint32_t s_addr = smem_u32(tiles + s * STAGE_BYTES);
           const uint32_t a_tmem = tmem + A_COL0 + s * A_COLS;
@@ -138,52 +171,64 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
             const uint32_t b_addr = s_addr + l * B_TILE;
 #pragma unroll
             for (int kk = 0; kk < TK / 32; ++kk)
-              mma_i8_ts(tmem + l * TJ, a_tmem + kk * 8, umma_desc_sw64(b_addr + kk * 32), IDESC,
+              if (!(dbg & 8)) mma_i8_ts(tmem + l * TJ, a_tmem + kk * 8, umma_desc_sw64(b_addr + kk * 32), IDESC,
                         (kt > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&sm.empty[s]);
+          mma_commit_mc(&sm.empty[s], CMASK);  // frees stage s in every CTA of the cluster
         }
         mma_commit(&sm.tfull);
       }
+      long long tot = 0;
+      TP_ACC(tot, t_all);
+      tp_flush(dbg, 0, 2, tot);
+      tp_flush(dbg, 0, 3, w_full);
+      tp_flush(dbg, 0, 4, w_tempty);
     }
   } else if (warp < 6) {
     // ---------------- one-hot producers: TMEM lane (i, b) <- [q_ik == b] for the stage's 64 k
+    // (one warp per lane quarter; kept branch-light: a lone warp per scheduler hides no latency)
     const int pl = (warp & 3) * 32 + lane;  // == TMEM lane (this warp's quarter)
     const int i = pl / NLEV, b = pl % NLEV;
     const int64_t row = r0 + i;
     const uint32_t bb = 0x01010101u * (uint32_t)b;
     const uint8_t* qrow = Q + (row < m ? row : 0) * n;
+    // k-tiles wholly inside [0, n) of a valid row load as 4 x 16 B when rows are 16-byte aligned
+    const int kvec = (row < m && (n & 15) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0)
+                         ? (int)(n / TK) : 0;
     auto load_codes = [&](int kt, uint4 (&v)[TK / 16]) {
+      if (kt < kvec) {
+        const uint4* src = reinterpret_cast<const uint4*>(qrow + (int64_t)kt * TK);
 #pragma unroll
-      for (int c = 0; c < TK / 16; ++c) {
-        const int64_t k = (int64_t)kt * TK + c * 16;
-        v[c] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (row < m) {
-          const uint8_t* src = qrow + k;
-          if (k + 16 <= n && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-            v[c] = __ldg(reinterpret_cast<const uint4*>(src));
-          } else {
-            uint8_t* vb = reinterpret_cast<uint8_t*>(&v[c]);
+        for (int c = 0; c < TK / 16; ++c) v[c] = __ldg(src + c);
+      } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) vb[q] = (k + q < n) ? src[q] : (uint8_t)0xFF;
+        for (int c = 0; c < TK / 16; ++c) {
+          uint8_t* vb = reinterpret_cast<uint8_t*>(&v[c]);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int64_t k = (int64_t)kt * TK + c * 16 + q;
+            vb[q] = (row < m && k < n) ? qrow[k] : (uint8_t)0xFF;
           }
         }
       }
     };
-    // byte-wise (x == b) -> 0x01 / 0x00 for codes < 16 or 0xFF: no borrow crosses a byte
+    // byte-wise (x == b) -> 0x80 / 0x00 for codes < 16 or 0xFF (no borrow crosses a byte):
+    // y = (x ^ b) | 0x80 per byte; its low 7 bits are zero iff x == b, so ~(y - 1) keeps bit 7
+    // exactly then.  The factor 128 of the u8 operand is divided out with the scale s_j.
     auto onehot = [&](uint32_t x) {
       const uint32_t y = (x ^ bb) | 0x80808080u;
-      return (~(y - 0x01010101u) & 0x80808080u) >> 7;
+      return (0x01010100u - y) & 0x80808080u;  // == ~(y - 0x01010101) & 0x80808080
     };
-    uint4 cur[TK / 16], nxt[TK / 16];
-    int jt = jt_lo, kt = 0;
-    if (jt < jt_hi) load_codes(kt, cur);
-    uint32_t ks = 0;
-    while (jt < jt_hi) {
-      const uint32_t s = ks % STAGES;
+    int jt = jt_lo, kt = 0, nk = ktiles_of(jt_lo);
+    uint32_t s = 0, ph = 0;
+    TP_T0(t_all);
+    long long w_empty = 0, w_st = 0;
+    // one stage: codes of this stage in cur (loaded a stage ago), prefetch the next into nxt
+    auto stage = [&](const uint4 (&cur)[TK / 16], uint4 (&nxt)[TK / 16]) -> bool {
+      if (jt >= jt_hi) return false;
       int jn = jt, kn = kt + 1;
-      if (kn >= ktiles_of(jn)) { ++jn; kn = 0; }
-      if (jn < jt_hi) load_codes(kn, nxt);  // prefetch the next stage's codes
+      if (kn >= nk) { ++jn; kn = 0; }
+      if (jn < jt_hi && !(dbg & 2)) load_codes(kn, nxt);
       uint32_t v[16];
 #pragma unroll
       for (int c = 0; c < TK / 16; ++c) {
@@ -192,42 +237,65 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         v[4 * c + 2] = onehot(cur[c].z);
         v[4 * c + 3] = onehot(cur[c].w);
       }
-      mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
+      TP_T0(t0);
+      mbar_wait(&sm.empty[s], ph ^ 1);
+      TP_ACC(w_empty, t0);
       tc_fence_after();
-      tmem_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS, v);
-      tmem_st_wait();
+      TP_T0(t2);
+      if (!(dbg & 2)) {
+        tmem_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS, v);
+        tmem_st_wait();
+      }
+      TP_ACC(w_st, t2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.full[s]);
-#pragma unroll
-      for (int c = 0; c < TK / 16; ++c) cur[c] = nxt[c];
+      if (jn != jt) nk += 2;  // ktiles_of(jt + 1) = ktiles_of(jt) + TJ / TK
       jt = jn;
       kt = kn;
-      ++ks;
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+      return true;
+    };
+    uint4 ca[TK / 16], cb[TK / 16];
+    if (jt < jt_hi) load_codes(kt, ca);
+    while (stage(ca, cb) && stage(cb, ca)) {
+    }
+    {
+      long long tot = 0;
+      TP_ACC(tot, t_all);
+      tp_flush(dbg, lane, 5, tot);
+      tp_flush(dbg, lane, 6, w_empty);
+      tp_flush(dbg, lane, 7, w_st);
     }
   } else {
-    // ---------------- epilogue
+    // ---------------- epilogue: two warps per TMEM lane quarter, each owning half the columns
     const int quarter = warp & 3;          // TMEM lane quarter of this warp
+    const int h = (warp - 6) >> 2;         // column half: chunks [2h, 2h + 2) of the j-tile
+    const int e = warp - 6;                // 0..7
     const int et = quarter * 32 + lane;    // 0..127 == TMEM lane == (i, b)
     const int i = et / NLEV, b = et % NLEV;
+    constexpr int EPI_THREADS = 256;
     double acc[NLEV];
 #pragma unroll
     for (int a = 0; a < NLEV; ++a) acc[a] = 0.0;
+    TP_T0(t_all);
+    long long e_sort = 0, e_wait = 0, e_drain = 0, e_walk = 0, e_bar = 0;
     for (int jt = jt_lo; jt < jt_hi; ++jt) {
       const int64_t J0 = (int64_t)jt * TJ;
+      TP_T0(ta);
       // (1) sorted order of each row's 32-column chunks (counting sort by code); overlaps MMA
-      constexpr int NTASK = (R * NCH + 3) / 4;
+      constexpr int NTASK = (R * NCH + 7) / 8;
       int codes[NTASK];
 #pragma unroll
       for (int u = 0; u < NTASK; ++u) {
-        const int task = quarter + 4 * u;
+        const int task = e + 8 * u;
         const int ri = task / NCH, c = task % NCH;
         const int64_t row = r0 + ri, j = J0 + c * 32 + lane;
         codes[u] = (task < R * NCH && row < m && j < n) ? (int)__ldg(Q + row * n + j) : 0xFF;
       }
 #pragma unroll
       for (int u = 0; u < NTASK; ++u) {
-        const int task = quarter + 4 * u;
+        const int task = e + 8 * u;
         if (task >= R * NCH) break;
         const int ri = task / NCH, c = task % NCH;
         const int code = codes[u];
@@ -244,13 +312,17 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         // invalid columns (j >= n, rows >= m) go after every segment
         sm.ipos[ri][c * 32 + lane] = (uint8_t)(pos >= 0 ? pos : 31);
       }
-      if (et < TJ) sm.scale[et] = (J0 + et < n) ? (float)scale[J0 + et] : 0.0f;
-      named_bar_sync(1, 128);
+      if (h == 0) sm.scale[et] = (J0 + et < n) ? (float)(scale[J0 + et] * (1.0 / 128.0)) : 0.0f;
+      named_bar_sync(1, EPI_THREADS);
+      TP_ACC(e_sort, ta);
+      TP_T0(tb0);
       // (2) drain: exact int32 digit sums -> fp32 (* s_j) into the staging tile, release TMEM
       mbar_wait(&sm.tfull, (jt - jt_lo) & 1);
+      TP_ACC(e_wait, tb0);
+      TP_T0(tc0);
       tc_fence_after();
 #pragma unroll 1
-      for (int g = 0; g < TJ / 16; ++g) {
+      for (int g = h * (TJ / 32); g < ((dbg & 4) ? 0 : (h + 1) * (TJ / 32)); ++g) {
         uint32_t d0[16], d1[16], d2[16];
         const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + g * 16;
         tmem_ld16(tb, d0);
@@ -268,10 +340,12 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.tempty);  // the next j-tile's MMAs may start now
+      TP_ACC(e_drain, tc0);
+      TP_T0(td0);
       // (3) segment sums over this thread's own (sorted) staging row: prefix sums in place,
       //     segment a of chunk c = P[off[a+1]] - P[off[a]]
 #pragma unroll 1
-      for (int c = 0; c < ((dbg & 1) ? 0 : NCH); ++c) {
+      for (int c = 2 * h; c < ((dbg & 1) ? 0 : 2 * h + 2); ++c) {
         float* row = &sm.stage[et][c * 32];
         float v[32];
 #pragma unroll
@@ -281,9 +355,9 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
 #pragma unroll
         for (int q = 0; q < 31; ++q) {
           p += v[q];
-          row[q + 1] = p;  // P[q + 1]; P[32] is never needed (segments end <= 31 < 32?)
+          row[q + 1] = p;  // P[q + 1]
         }
-        const float ptot = p + v[31];
+        const float ptot = p + v[31];  // P[32]
 #pragma unroll
         for (int a = 0; a < NLEV; ++a) {
           const int s0 = sm.off[i][c][a], s1 = sm.off[i][c][a + 1];
@@ -292,16 +366,37 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           acc[a] += (s1 > s0) ? (double)(hi - lo) : 0.0;
         }
       }
-      named_bar_sync(1, 128);  // perm/off/scale/stage are rewritten for the next j-tile
+      TP_ACC(e_walk, td0);
+      TP_T0(te0);
+      named_bar_sync(1, EPI_THREADS);  // ipos/off/scale/stage are rewritten for the next j-tile
+      TP_ACC(e_bar, te0);
     }
-    const int64_t row = r0 + i;
-    if (row < m) {
+    {
+      long long tot = 0;
+      TP_ACC(tot, t_all);
+      tp_flush(dbg, lane, 8, tot);
+      tp_flush(dbg, lane, 9, e_sort);
+      tp_flush(dbg, lane, 10, e_wait);
+      tp_flush(dbg, lane, 11, e_drain);
+      tp_flush(dbg, lane, 12, e_walk);
+      tp_flush(dbg, lane, 13, e_bar);
+    }
+    // the two halves' partial sums meet in the (now free) staging tile, in a fixed order
+    double* red = reinterpret_cast<double*>(&sm.stage[0][0]);
+    if (h == 1) {
 #pragma unroll
-      for (int a = 0; a < NLEV; ++a) Cpart[(row * NLEV + a) * NLEV + b] = acc[a];
+      for (int a = 0; a < NLEV; ++a) red[et * NLEV + a] = acc[a];
+    }
+    named_bar_sync(1, EPI_THREADS);
+    const int64_t row = r0 + i;
+    if (h == 0 && row < m) {
+#pragma unroll
+      for (int a = 0; a < NLEV; ++a) Cpart[(row * NLEV + a) * NLEV + b] = acc[a] + red[et * NLEV + a];
     }
   }
   tc_fence_before();
   __syncthreads();
+  cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
@@ -363,7 +458,7 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   CUtensorMap tmap;
   cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)(3 * P)};
   cuuint64_t strides[1] = {(cuuint64_t)P};
-  cuuint32_t box[2] = {TK, TJ};  // 64 k (bytes) x 128 j
+  cuuint32_t box[2] = {TK, SLICE};  // 64 k (bytes) x TJ / CS j: one CTA's slice
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)Hq, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -388,10 +483,38 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
     bnd[p - 1] = jt;
   }
   const int4 jsplit = make_int4(bnd[0], bnd[1], bnd[2], 0);
-  const unsigned groups = (unsigned)((m + R - 1) / R);
+  const int groups = (int)((m + R - 1) / R);
+  const int gp = (groups + CS - 1) / CS * CS;  // whole clusters; extra CTAs own no rows
   static const int dbg = getenv("GANQ_TGRAM_DBG") ? atoi(getenv("GANQ_TGRAM_DBG")) : 0;
-  tgram_tc_kernel<NLEV><<<SPLIT * groups, THREADS, smem, st>>>(tmap, Q, scale, m, n, P, jsplit, Cg, dbg);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(SPLIT * gp));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GANQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, tgram_tc_kernel<NLEV>, tmap, Q, scale, m, n, P, jsplit, gp, Cg, dbg));
   GANQ_LAUNCH_CHECK("tgram_tc_kernel");
+  if (dbg & 16) {
+    unsigned long long h[16];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_tgprof, sizeof(h));
+    const double c = (double)(SPLIT * gp);
+    fprintf(stderr,
+            "tgprof per CTA (kcyc): tma %.1f (wait empty %.1f) | mma %.1f (wait full %.1f, tempty %.1f) | "
+            "prod/warp %.1f (wait empty %.1f, st %.1f) | epi/warp %.1f (sort %.1f, wait tfull %.1f, drain %.1f, "
+            "walk %.1f, bar %.1f)\n",
+            h[0] / c / 1e3, h[1] / c / 1e3, h[2] / c / 1e3, h[3] / c / 1e3, h[4] / c / 1e3, h[5] / c / 4e3,
+            h[6] / c / 4e3, h[7] / c / 4e3, h[8] / c / 8e3, h[9] / c / 8e3, h[10] / c / 8e3, h[11] / c / 8e3,
+            h[12] / c / 8e3, h[13] / c / 8e3);
+    const unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_tgprof, z, sizeof(z));
+  }
   return GANQ_OK;
 }
 

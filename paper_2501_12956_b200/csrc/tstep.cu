@@ -242,11 +242,9 @@ __global__ void init_codebook_kernel(const float* __restrict__ W, int64_t m, int
 }
 
 template <int NLEV>
-ganq_status_t launch_tstep_t(const double* H, const int8_t* Hq, const double* qscale, const float* WH,
-                             const uint8_t* Q, int64_t m, int64_t n, int empty_rule, float* T, double* G,
-                             double* Dv, double* b, int* cnt, int* fb, cudaStream_t st) {
-  ganq_status_t s = launch_tgram_tc(Hq, qscale, Q, m, n, NLEV, G, st);
-  if (s) return s;
+ganq_status_t launch_tsolve_t(const double* H, const float* WH, const uint8_t* Q, int64_t m, int64_t n,
+                              int empty_rule, float* T, double* G, double* Dv, double* b, int* cnt, int* fb,
+                              cudaStream_t st) {
   trhs_kernel<NLEV><<<(unsigned)((m + 7) / 8), 256, 0, st>>>(H, WH, Q, m, n, Dv, b, cnt);
   GANQ_LAUNCH_CHECK("trhs_kernel");
   tsolve_kernel<NLEV><<<(unsigned)((m + 7) / 8), 256, 0, st>>>(G, Dv, b, cnt, m, empty_rule, T, fb);
@@ -266,16 +264,16 @@ ganq_status_t launch_init_codebook(const float* W, int64_t m, int64_t n, int nle
   return GANQ_OK;
 }
 
-ganq_status_t launch_tstep(const double* H, const int8_t* Hq, const double* qscale, const float* WH,
-                           const uint8_t* Q, int64_t m, int64_t n, int nlev, int empty_rule, float* T,
-                           double* G, double* Dv, double* b, int* cnt, int* fb, cudaStream_t st) {
+ganq_status_t launch_tsolve(const double* H, const float* WH, const uint8_t* Q, int64_t m, int64_t n, int nlev,
+                            int empty_rule, float* T, double* G, double* Dv, double* b, int* cnt, int* fb,
+                            cudaStream_t st) {
   switch (nlev) {
-    case 2: return launch_tstep_t<2>(H, Hq, qscale, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
-    case 4: return launch_tstep_t<4>(H, Hq, qscale, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
-    case 8: return launch_tstep_t<8>(H, Hq, qscale, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
-    case 16: return launch_tstep_t<16>(H, Hq, qscale, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 2: return launch_tsolve_t<2>(H, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 4: return launch_tsolve_t<4>(H, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 8: return launch_tsolve_t<8>(H, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 16: return launch_tsolve_t<16>(H, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
     default:
-      set_error(GANQ_ERR_UNSUPPORTED, "tstep: 2^N = %d levels unsupported (N must be 1..4)", nlev);
+      set_error(GANQ_ERR_UNSUPPORTED, "tsolve: 2^N = %d levels unsupported (N must be 1..4)", nlev);
       return GANQ_ERR_UNSUPPORTED;
   }
 }
