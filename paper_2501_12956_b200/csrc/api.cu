@@ -79,7 +79,7 @@ struct StageScope {
 namespace {
 
 struct Layout {
-  size_t A64, Lhat, LThi, LTlo, Ehi, Elo, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, Xhi, Xlo, Hhi,
+  size_t A64, Lhat, LTq, tL, Eq, sE, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, Xhi, Xlo, Hhi,
       Hlo, status, mean, per_row, total_d, end;
 };
 
@@ -95,10 +95,11 @@ Layout make_layout(int64_t m, int64_t n, int nlev) {
   L.A64 = take(nn * sizeof(double));
   const size_t np = (size_t)ss_pitch(n);
   L.Lhat = take((size_t)n * np * sizeof(float));
-  L.LThi = take((size_t)n * np * sizeof(float));
-  L.LTlo = take((size_t)n * np * sizeof(float));
-  L.Ehi = take((size_t)m * np * sizeof(float));
-  L.Elo = take((size_t)m * np * sizeof(float));
+  const size_t npq = (size_t)ssq_pitch(n), nblk = npq / 64, mq = ((size_t)m + 31) / 32 * 32;
+  L.LTq = take(3 * (size_t)n * npq);               // int8 digits of LhatT (R-15)
+  L.tL = take(nblk * (size_t)n * sizeof(float));   // their per (block, column) scales
+  L.Eq = take(3 * (size_t)m * npq);                // int8 digits of the residuals E
+  L.sE = take(nblk * mq * sizeof(float));          // their per (block, row) scales
   L.H32 = take(nn * sizeof(float));
   L.WH = take(mn * sizeof(float));
   L.E = take(mn * sizeof(float));
@@ -322,9 +323,11 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
   {
     GANQ_STAGE(ST_DERIVE);
     if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
-    if ((s = launch_lhat_split(at<double>(ws, L.A64), n, Lhat, at<float>(ws, L.LThi), at<float>(ws, L.LTlo),
-                               st)))
+    if ((s = launch_lhat_prep(at<double>(ws, L.A64), n, Lhat, at<int8_t>(ws, L.LTq), at<float>(ws, L.tL), st)))
       return s;
+    // block scales of rows >= m are never written but are read (multiplied by zero digits)
+    GANQ_CUDA_TRY(cudaMemsetAsync(at<float>(ws, L.sE), 0,
+                                  (size_t)ssq_pitch(n) / 64 * (((size_t)m + 31) / 32 * 32) * sizeof(float), st));
   }
   {
     // fixed-point int8 digits of H's strict lower triangle for the tensor-core T-update
@@ -355,8 +358,8 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
     {
       // S-update
       GANQ_STAGE(ST_SSTEP);
-      if ((s = launch_sstep_tc(W, Lhat, at<float>(ws, L.LThi), at<float>(ws, L.LTlo), T, m, n, nlev, Q,
-                               at<float>(ws, L.Ehi), at<float>(ws, L.Elo), st)))
+      if ((s = launch_sstep_tc(W, Lhat, at<int8_t>(ws, L.LTq), at<float>(ws, L.tL), T, m, n, nlev, Q,
+                               at<int8_t>(ws, L.Eq), at<float>(ws, L.sE), st)))
         return s;
     }
     {

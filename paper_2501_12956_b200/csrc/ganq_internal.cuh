@@ -53,12 +53,12 @@ ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* sca
 ganq_status_t launch_tgram_tc(const int8_t* Hq, const double* scale, const uint8_t* Q, int64_t m,
                               int64_t n, int nlev, double* Cg, cudaStream_t st);
 // sstep_tc.cu
-int64_t ss_pitch(int64_t n);
-ganq_status_t launch_lhat_split(const double* L, int64_t n, float* Lhat, float* LThi, float* LTlo,
-                                cudaStream_t st);
-ganq_status_t launch_sstep_tc(const float* W, const float* Lhat, const float* LThi, const float* LTlo,
-                              const float* T, int64_t m, int64_t n, int nlev, uint8_t* Q, float* Ehi,
-                              float* Elo, cudaStream_t st);
+int64_t ss_pitch(int64_t n);   // fp32 Lhat row pitch (multiple of 4)
+int64_t ssq_pitch(int64_t n);  // int8 digit-plane row pitch (multiple of 64); n_blocks = ssq_pitch / 64
+ganq_status_t launch_lhat_prep(const double* L, int64_t n, float* Lhat, int8_t* LTq, float* tL, cudaStream_t st);
+ganq_status_t launch_sstep_tc(const float* W, const float* Lhat, const int8_t* LTq, const float* tL,
+                              const float* T, int64_t m, int64_t n, int nlev, uint8_t* Q, int8_t* Eq,
+                              float* sE, cudaStream_t st);
 // gemm_tc.cu
 int64_t gemm_pitch(int64_t K);
 ganq_status_t launch_split_tf32(const float* X, int64_t rows, int64_t K, float* hi, float* lo,
@@ -111,6 +111,23 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, ui
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
       "%4}], [%2];" ::"r"(smem_u32(smem_dst)),
       "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// TMA 3D tile load (coordinates innermost first); out-of-range boxes are zero-filled.
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const void* tmap, uint64_t* bar, int c0,
+                                               int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
       : "memory");
 }
 // TMA 2D tile load multicast to the CTAs of `mask` in the cluster (same smem offsets and
@@ -336,6 +353,17 @@ __host__ __device__ constexpr uint32_t umma_idesc(uint32_t ab_format, uint32_t a
          (b_mn_major << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 // kind::i8: signed int8 A and B (format 1), S32 accumulator (c_format 2), K-major operands.
+// K-major SWIZZLE_64B UMMA smem descriptor: 64-byte rows, 8-row atoms of 512 B (SBO),
+// layout type 4 (the TMA SWIZZLE_64B image of a box with a 64-byte inner extent).
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(16 >> 4) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
 __host__ __device__ constexpr uint32_t umma_idesc_s8(uint32_t M, uint32_t N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }

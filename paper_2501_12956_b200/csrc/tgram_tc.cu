@@ -50,17 +50,6 @@ constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile 
 constexpr uint32_t IDESC = umma_idesc_u8s8(128, TJ);  // A = one-hot bytes 0 / 128 (u8)
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
 
-// SW64 K-major UMMA descriptor: 64-byte rows, 8-row atoms of 512 B (SBO), layout type 4.
-__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)(16 >> 4) << 16;
-  d |= (uint64_t)(512 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;
-  return d;
-}
-
 // debug-only cycle accounting per warp role (GANQ_TGRAM_DBG & 16)
 __device__ unsigned long long g_tgprof[16];
 #define TP_T0(v) long long v = (dbg & 16) ? clock64() : 0
