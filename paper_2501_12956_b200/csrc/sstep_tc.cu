@@ -20,7 +20,7 @@
 // finished 64-column half of residuals for the tensor cores.
 //
 // Warps: 0 = TMA producer, 1 = MMA issuer (+TMEM owner), 2-5 = TMEM readers (one lane
-// quarter each), 6-9 = panel group (4 lanes per row).
+// quarter each), 6 = decisions (lane = row), 7-9 = in-panel feedback, code and digit stores.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -36,6 +36,8 @@ namespace {
 
 constexpr int RB = 32;              // rows per CTA (UMMA N)
 constexpr int PW = 128;             // panel width (UMMA M)
+constexpr int SB = 8;               // decision sub-panel width
+constexpr int NSUB = PW / SB;
 constexpr int UB = 64;              // u per feedback block (64-byte SW64 rows of int8 digits)
 constexpr int STAGES = 3;
 constexpr int NBUF = 4;             // TMEM accumulator sets of 3 x 32 columns (weights 2^16, 2^8, 1)
@@ -57,17 +59,25 @@ __host__ __device__ constexpr bool prod_first(int p) { return p == 0 || p == 1 |
 struct SsSmem {
   alignas(128) float Ld[PW][PW];         // Lhat[jb + c][jb + c2] of the current panel (TMA)
   alignas(16) float As[2][PW][RB + 1];   // drained feedback per (panel column, row), 2 buffers
-  alignas(16) float es[2 * 32][RB + 1];  // residuals of the current half panel (column, row)
-  alignas(16) uint8_t cs[32][RB + 4];    // codes of the current sub-panel (column, row)
+  alignas(16) float es[PW][RB + 1];      // residuals of the current panel (column, row)
+  alignas(16) uint8_t cs[PW][RB + 4];    // codes of the current panel (column, row)
+  alignas(16) float ws[PW][RB + 1];      // weights of the current panel (column, row)
+  alignas(16) float sEn[2][RB];          // E block scales of the newest source panel (2 halves)
   alignas(8) uint64_t full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF];
   alignas(8) uint64_t acc_ready[2], as_free[2], ebar, ldbar;
   uint32_t tmem_slot;
 };
 
-// debug-only cycle accounting per warp role (GANQ_SSTEP_DBG & 16)
+// debug-only cycle accounting per warp role: compiled with -DGANQ_KPROF, enabled at run time
+// by GANQ_SSTEP_DBG & 16 (tools/ss_prof.sh); absent from the default build
 __device__ unsigned long long g_ssprof[16];
+#ifdef GANQ_KPROF
 #define TP_T0(v) long long v = (dbg & 16) ? clock64() : 0
 #define TP_ACC(acc, v) do { if (dbg & 16) acc += clock64() - v; } while (0)
+#else
+#define TP_T0(v) constexpr long long v = 0
+#define TP_ACC(acc, v) do { (void)(acc); (void)(v); } while (0)
+#endif
 __device__ __forceinline__ void tp_flush(int dbg, int lane, int slot, long long v) {
   if ((dbg & 16) && lane == 0) atomicAdd(&g_ssprof[slot], (unsigned long long)v);
 }
@@ -95,6 +105,21 @@ __device__ __forceinline__ void argmin_tree(float z, const float (&t)[NLEV], int
   }
   q = idx[0];
   tq = tv[0];
+}
+
+// Sorted-codebook selection: with thresholds th sorted ascending, the predicates p_s = z > th_s
+// are monotone, so the selected position is found by a balanced tree of selects on p (depth
+// log2 NLEV, no count or index arithmetic on the dependency chain).
+template <int LO, int HI, typename V, int NLEV>
+__device__ __forceinline__ V tree_select(const V (&v)[NLEV], const bool (&p)[NLEV > 1 ? NLEV - 1 : 1]) {
+  if constexpr (LO == HI) {
+    return v[LO];
+  } else {
+    constexpr int MID = (LO + HI) / 2;
+    const V lo = tree_select<LO, MID>(v, p);
+    const V hi = tree_select<MID + 1, HI>(v, p);
+    return p[MID] ? hi : lo;
+  }
 }
 
 __device__ __forceinline__ void fence_proxy_async_global() {
@@ -233,25 +258,35 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         for (int k2 = 0; k2 < PW / UB; ++k2, ++kb) {
           const uint32_t buf = kb % NBUF;
           const int64_t blk = (npq - (int64_t)PW * (qs + 1)) / UB + k2;  // storage block of u
+          // block scales: LhatT per (column, block), E per (row, block); the digit weights of the
+          // three groups are 2^32, 2^24, 2^16 = 2^16 x (65536, 256, 1).  Scales of older source
+          // panels are read before the wait; those of the newest one (qs = q - 1) come from the
+          // panel group's shared copy after tfull (ordered after its stores by ebar -> TMA ->
+          // MMA -> commit).
+          const float tl = (j >= 0) ? __ldg(tL + blk * n + j) * 65536.0f : 0.0f;
+          float se[RB];
+          const bool newest = (qs == q - 1);
+          if (!newest) {
+            const float4* sp4 = reinterpret_cast<const float4*>(sE + blk * ((m + RB - 1) / RB * RB) + r0);
+#pragma unroll
+            for (int r4 = 0; r4 < RB / 4; ++r4) {
+              const float4 v4 = sp4[r4];
+              se[4 * r4 + 0] = v4.x;
+              se[4 * r4 + 1] = v4.y;
+              se[4 * r4 + 2] = v4.z;
+              se[4 * r4 + 3] = v4.w;
+            }
+          }
           TP_T0(t0);
           mbar_wait(&sm.tfull[buf], (kb / NBUF) & 1);
           TP_ACC(w_tf, t0);
           tc_fence_after();
-          // block scales: LhatT per (column, block), E per (row, block); the digit weights of the
-          // three groups are 2^32, 2^24, 2^16 = 2^16 x (65536, 256, 1)
-          const float tl = (j >= 0) ? tL[blk * n + j] * 65536.0f : 0.0f;
-          float se[RB];
-          const float4* sp4 = reinterpret_cast<const float4*>(sE + blk * ((m + RB - 1) / RB * RB) + r0);
+          if (newest) {
 #pragma unroll
-          for (int r4 = 0; r4 < RB / 4; ++r4) {
-            const float4 v = sp4[r4];  // written by this CTA's panel group: no __ldg
-            se[4 * r4 + 0] = v.x * tl;
-            se[4 * r4 + 1] = v.y * tl;
-            se[4 * r4 + 2] = v.z * tl;
-            se[4 * r4 + 3] = v.w * tl;
+            for (int r = 0; r < RB; ++r) se[r] = sm.sEn[k2][r];
           }
-          // (read after tfull: the E scales of the panel just decided are stored by the panel group
-          // before ebar, which orders them before this block's TMA, MMA and commit)
+#pragma unroll
+          for (int r = 0; r < RB; ++r) se[r] *= tl;
           const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BUF_COLS;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {  // rows [16 hh, 16 hh + 16): three weight groups
@@ -288,216 +323,290 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     tp_flush(dbg, lane, 7, w_tf);
     tp_flush(dbg, lane, 8, w_af);
   } else {
-    // ---------------- panel group (warps 6-9): 4 lanes per row, sequential decisions.
-    // Lane (r, sub) holds levels [4 sub, 4 sub + 4) of row r's codebook and the accumulators
-    // of the sub-panel columns c = 4 k + sub.  Per column: the owner lane's z and w are
-    // broadcast, each lane takes the argmin over its 4 levels, two shuffle rounds combine the
-    // candidates (distance, then index: the first index wins ties exactly as in a sequential
-    // strict '<' scan), and every lane forms e = w - t_q and updates its own accumulators.
-    constexpr int LPL = NLEV / 4 > 0 ? NLEV / 4 : 1;   // levels per lane
-    const int pl = threadIdx.x - 192;                  // 0..127
-    const int rr = pl >> 2, sub = pl & 3;              // row within CTA, quarter
-    const int64_t row = r0 + rr;
-    const bool live = row < m;
-    const unsigned gmask = 0xffffffffu;
-    const int gbase = lane & ~3;                       // first lane of this row's group
-    const int64_t mq = (m + RB - 1) / RB * RB;         // rows of the sE table
-    float t[LPL];
+    // ---------------- panel group (warps 6-9).  Warp 6 decides (lane = row); warps 7-9 apply
+    // the feedback between sub-panels (the next sub-panel's first, handed over by a named
+    // barrier), store the codes and quantize finished halves of residuals for the tensor cores.
+    const int64_t mq = (m + RB - 1) / RB * RB;  // rows of the sE table
+    // named barriers: the panel end, and per sub-panel parity (the decision warp may run two
+    // sub-panels ahead of the helpers and vice versa, so each id has one open phase at most)
+    constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_X = 6;  // ES: 4, 5; X: 6, 7
+    if (warp == 6) {
+      // ===== decision warp.  The row's codebook sorted (stable by index); th[s] separates
+      // sorted positions s and s + 1: the midpoint of two distinct values (a tie goes to the
+      // lower original index), or, inside a run of equal values, the next boundary above, so
+      // that q = #{s : z > th_s} lands on the first member of the nearest run.  This is the
+      // argmin of Eq. 22 with first-index ties, up to the rounding of the midpoints (R-10);
+      // the position is read off the monotone predicates z > th_s by a select tree.
+      const int64_t row = r0 + lane;
+      const bool live = row < m;
+      float v[NLEV];
+      int ix[NLEV];
 #pragma unroll
-    for (int x = 0; x < LPL; ++x) {
-      const int lev = sub * LPL + x;
-      t[x] = (live && lev < NLEV) ? T[row * NLEV + lev] : 0.0f;
-    }
-    const float* wrow = W + (live ? row : 0) * n;
-    const uint32_t pbar = 3;                           // named barrier of the panel group
-    TP_T0(t_all);
-    long long w_acc = 0, w_ld = 0, c_dec = 0, c_st = 0, c_x = 0, c_bar = 0;
-    for (int q = 0; q < P; ++q) {
-      const int64_t jb = n - (int64_t)PW * (q + 1);
-      const int ab = q & 1;
-      TP_T0(t0);
-      mbar_wait(&sm.acc_ready[ab], (q >> 1) & 1);
-      TP_ACC(w_acc, t0);
-      TP_T0(t1);
-      mbar_wait(&sm.ldbar, q & 1);
-      TP_ACC(w_ld, t1);
-      float wn[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int64_t j = jb + 32 * (PW / 32 - 1) + 4 * k + sub;
-        wn[k] = (j >= 0) ? wrow[j] : 0.0f;
+      for (int s2 = 0; s2 < NLEV; ++s2) {
+        v[s2] = live ? T[row * NLEV + s2] : 0.0f;
+        ix[s2] = s2;
       }
+#pragma unroll
+      for (int pass = 0; pass < NLEV; ++pass)
+#pragma unroll
+        for (int s2 = pass & 1; s2 + 1 < NLEV; s2 += 2) {
+          const bool sw = v[s2] > v[s2 + 1] || (v[s2] == v[s2 + 1] && ix[s2] > ix[s2 + 1]);
+          const float tv = v[s2];
+          const int ti = ix[s2];
+          v[s2] = sw ? v[s2 + 1] : v[s2];
+          ix[s2] = sw ? ix[s2 + 1] : ix[s2];
+          v[s2 + 1] = sw ? tv : v[s2 + 1];
+          ix[s2 + 1] = sw ? ti : ix[s2 + 1];
+        }
+      int rfirst[NLEV];  // original index of the first member of each position's run
+#pragma unroll
+      for (int s2 = 0; s2 < NLEV; ++s2) rfirst[s2] = (s2 > 0 && v[s2] == v[s2 - 1]) ? rfirst[s2 - 1] : ix[s2];
+      uint64_t pk = 0;  // original index of each sorted position, 4 bits each
+#pragma unroll
+      for (int s2 = 0; s2 < NLEV; ++s2) pk |= (uint64_t)ix[s2] << (4 * s2);
+      int pos[NLEV];  // sorted positions (constants: selected without registers)
+#pragma unroll
+      for (int s2 = 0; s2 < NLEV; ++s2) pos[s2] = s2;
+      constexpr int NT = NLEV - 1;
+      float th[NT];
+      float above = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int s2 = NT - 1; s2 >= 0; --s2) {
+        if (v[s2] == v[s2 + 1]) {
+          th[s2] = above;
+        } else {
+          const float mid = __fmul_rn(0.5f, __fadd_rn(v[s2], v[s2 + 1]));
+          // z == mid is a tie: the upper run wins it iff its first index is lower (z >= mid)
+          th[s2] = (ix[s2 + 1] < rfirst[s2]) ? nextafterf(mid, -__int_as_float(0x7f800000)) : mid;
+          above = th[s2];
+        }
+      }
+      named_bar_sync(BAR_PANEL, 128);  // the helpers staged panel 0's weights
+      TP_T0(t_all);
+      long long w_acc = 0, w_ld = 0, c_dec = 0, c_bar = 0;
+      for (int q = 0; q < P; ++q) {
+        const int64_t jb = n - (int64_t)PW * (q + 1);
+        const int ab = q & 1;
+        TP_T0(t0);
+        mbar_wait(&sm.acc_ready[ab], (q >> 1) & 1);
+        TP_ACC(w_acc, t0);
+        TP_T0(t1);
+        mbar_wait(&sm.ldbar, q & 1);
+        TP_ACC(w_ld, t1);
+        float a2[SB];  // feedback of the sub-panel being decided into the next one (sp - 1)
 #pragma unroll 1
-      for (int sp = PW / 32 - 1; sp >= 0; --sp) {
-        const int64_t j0 = jb + 32 * sp;     // first column of the sub-panel (may be < 0)
-        float (*esp)[RB + 1] = &sm.es[32 * (sp & 1)];  // this sub-panel's half of es
-        float a[8], w[8];
+        for (int sp = NSUB - 1; sp >= 0; --sp) {
+          const int64_t j0 = jb + SB * sp;  // first column of the sub-panel (may be < 0)
+          TP_T0(tb);
+          // the helpers' feedback from sub-panels >= sp + 2 into sp (none for the first two)
+          if (sp < NSUB - 2) named_bar_sync(BAR_X + (sp & 1), 128);
+          TP_ACC(c_bar, tb);
+          TP_T0(t2);
+          float a[SB], w[SB], ev[SB];
+          int iv[SB];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          a[k] = sm.As[ab][32 * sp + 4 * k + sub][rr];
-          w[k] = wn[k];
+          for (int k = 0; k < SB; ++k) {
+            a[k] = sm.As[ab][SB * sp + k][lane];
+            if (sp < NSUB - 1) a[k] += a2[k];
+            a2[k] = 0.0f;
+            w[k] = sm.ws[SB * sp + k][lane];
+          }
+#pragma unroll
+          for (int cc = SB - 1; cc >= 0; --cc) {
+            const float z = __fadd_rn(w[cc], a[cc]);
+            bool pz[NT > 0 ? NT : 1];
+#pragma unroll
+            for (int s2 = 0; s2 < NT; ++s2) pz[s2] = z > th[s2];
+            const float tq = tree_select<0, NLEV - 1>(v, pz);
+            const int iq = (int)((pk >> (4 * tree_select<0, NLEV - 1>(pos, pz))) & 15u);
+            const float ec = (j0 + cc >= 0) ? __fsub_rn(w[cc], tq) : 0.0f;
+            ev[cc] = ec;  // stored after the sub-panel: no shared stores between the Ld loads
+            iv[cc] = iq;
+            // in-sub-panel feedback into the columns left of cc (entries >= cc are already used)
+            const float4* lrow = reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][SB * sp]);
+#pragma unroll
+            for (int k4 = 0; k4 < SB / 4; ++k4) {
+              if (4 * k4 < cc) {
+                const float4 l = lrow[k4];
+                a[4 * k4 + 0] = fmaf(ec, l.x, a[4 * k4 + 0]);
+                a[4 * k4 + 1] = fmaf(ec, l.y, a[4 * k4 + 1]);
+                a[4 * k4 + 2] = fmaf(ec, l.z, a[4 * k4 + 2]);
+                a[4 * k4 + 3] = fmaf(ec, l.w, a[4 * k4 + 3]);
+              }
+            }
+            // ... and into the next sub-panel
+            if (sp > 0) {
+              const float4* lnext = reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][SB * (sp - 1)]);
+#pragma unroll
+              for (int k4 = 0; k4 < SB / 4; ++k4) {
+                const float4 l = lnext[k4];
+                a2[4 * k4 + 0] = fmaf(ec, l.x, a2[4 * k4 + 0]);
+                a2[4 * k4 + 1] = fmaf(ec, l.y, a2[4 * k4 + 1]);
+                a2[4 * k4 + 2] = fmaf(ec, l.z, a2[4 * k4 + 2]);
+                a2[4 * k4 + 3] = fmaf(ec, l.w, a2[4 * k4 + 3]);
+              }
+            }
+          }
+#pragma unroll
+          for (int cc = 0; cc < SB; ++cc) {
+            sm.es[SB * sp + cc][lane] = ev[cc];
+            sm.cs[SB * sp + cc][lane] = (uint8_t)iv[cc];
+          }
+          TP_ACC(c_dec, t2);
+          __syncwarp();
+          named_bar_arrive(BAR_ES + (sp & 1), 128);  // es / cs of sub-panel sp are complete
         }
-        TP_T0(t2);
-        if (sp > 0) {  // prefetch the next sub-panel's weights
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int64_t j = j0 - 32 + 4 * k + sub;
-            wn[k] = (j >= 0) ? wrow[j] : 0.0f;
-          }
-        }
-#pragma unroll
-        for (int cc = 31; cc >= 0; --cc) {
-          const int own = cc & 3, kc = cc >> 2;
-          const float zl = __fadd_rn(w[kc], a[kc]);                       // valid on the owner
-          const float z = __shfl_sync(gmask, zl, gbase | own);
-          const float wc = __shfl_sync(gmask, w[kc], gbase | own);
-          // local argmin over this lane's levels (first index on ties)
-          float bd = fabsf(__fsub_rn(z, t[0]));
-          int bi = sub * LPL;
-          float bt = t[0];
-#pragma unroll
-          for (int x = 1; x < LPL; ++x) {
-            const float d = fabsf(__fsub_rn(z, t[x]));
-            const bool better = d < bd;
-            bd = better ? d : bd;
-            bi = better ? sub * LPL + x : bi;
-            bt = better ? t[x] : bt;
-          }
-          if (NLEV < 4 && sub * LPL >= NLEV) bd = __int_as_float(0x7f800000);  // no levels here
-#pragma unroll
-          for (int o = 1; o < 4; o <<= 1) {
-            const float od = __shfl_xor_sync(gmask, bd, o);
-            const int oi = __shfl_xor_sync(gmask, bi, o);
-            const float ot = __shfl_xor_sync(gmask, bt, o);
-            const bool take = (od < bd) || (od == bd && oi < bi);
-            bd = take ? od : bd;
-            bi = take ? oi : bi;
-            bt = take ? ot : bt;
-          }
-          const bool real = j0 + cc >= 0;
-          const float ec = real ? __fsub_rn(wc, bt) : 0.0f;
-          if (sub == own) {
-            esp[cc][rr] = ec;
-            sm.cs[cc][rr] = (uint8_t)bi;
-          }
-          const float* lrow = &sm.Ld[32 * sp + cc][32 * sp + sub];  // Lhat[j][j0 + 4 k + sub]
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (4 * k + sub < cc) a[k] = fmaf(ec, lrow[4 * k], a[k]);
-        }
-        TP_ACC(c_dec, t2);
         TP_T0(t3);
-        named_bar_sync(pbar, 128);  // es / cs of this sub-panel complete
+        named_bar_sync(BAR_PANEL, 128);  // the helpers finished the panel
         TP_ACC(c_bar, t3);
-        TP_T0(t4);
-        // codes: lane sub writes columns [8 sub, 8 sub + 8) of its row
-        if (live) {
-          uint8_t cv[8];
+      }
+      long long tot = 0;
+      TP_ACC(tot, t_all);
+      tp_flush(dbg, lane, 9, tot);
+      tp_flush(dbg, lane, 10, w_acc);
+      tp_flush(dbg, lane, 11, w_ld);
+      tp_flush(dbg, lane, 12, c_dec);
+      tp_flush(dbg, lane, 15, c_bar);
+    } else {
+      // ===== helpers: lane = row.  After sub-panel sp is decided, its residuals are applied to
+      // every column of sub-panels <= sp - 2 (4-column chunks dealt round-robin to the warps);
+      // codes leave in 32-column groups, residual digits in 64-column halves.
+      const int hw = warp - 7;
+      const int rr = lane;
+      const int64_t row = r0 + rr;
+      const bool live = row < m;
+      const float* wrow = W + (live ? row : 0) * n;
+      // weights of panel columns [c0, c0 + SB) of the panel starting at jb -> ws (lane = row)
+      // (asynchronous copies: they complete while the decisions go on, waited for at panel end)
+      auto stage_w = [&](int64_t jbp, int c0) {
 #pragma unroll
-          for (int x = 0; x < 8; ++x) cv[x] = sm.cs[8 * sub + x][rr];
-          const int64_t jj = j0 + 8 * sub;
-          uint8_t* qd = Q + row * n + jj;
-          if (jj >= 0 && (reinterpret_cast<uintptr_t>(qd) & 7) == 0) {
-            uint2 pk;
-            pk.x = cv[0] | (cv[1] << 8) | (cv[2] << 16) | ((uint32_t)cv[3] << 24);
-            pk.y = cv[4] | (cv[5] << 8) | (cv[6] << 16) | ((uint32_t)cv[7] << 24);
-            *reinterpret_cast<uint2*>(qd) = pk;
-          } else {
+        for (int k = 0; k < SB; ++k) {
+          const int64_t j = jbp + c0 + k;
+          if (live && j >= 0)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(&sm.ws[c0 + k][rr])),
+                         "l"(wrow + j) : "memory");
+          else
+            sm.ws[c0 + k][rr] = 0.0f;
+        }
+      };
+      for (int c0 = hw * SB; c0 < PW; c0 += 3 * SB) stage_w(n - PW, c0);
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      named_bar_sync(BAR_PANEL, 128);
+      TP_T0(t_all);
+      long long c_x = 0, c_st = 0;
+      for (int q = 0; q < P; ++q) {
+        const int64_t jb = n - (int64_t)PW * (q + 1);
+        const int ab = q & 1;
+        mbar_wait(&sm.acc_ready[ab], (q >> 1) & 1);
+        mbar_wait(&sm.ldbar, q & 1);
+#pragma unroll 1
+        for (int sp = NSUB - 1; sp >= 0; --sp) {
+          named_bar_sync(BAR_ES + (sp & 1), 128);  // the decision warp finished sub-panel sp
+          TP_T0(t4);
+          if (sp >= 2) {
+            float e8[SB];
+#pragma unroll
+            for (int cc = 0; cc < SB; ++cc) e8[cc] = sm.es[SB * sp + cc][rr];
+            const int nch = SB * (sp - 1) / 4;  // 4-column chunks of the columns [0, SB (sp - 1))
+#pragma unroll 1
+            for (int c4 = hw; c4 < nch; c4 += 3) {
+              float acc[4];
+#pragma unroll
+              for (int y = 0; y < 4; ++y) acc[y] = sm.As[ab][4 * c4 + y][rr];
+#pragma unroll
+              for (int cc = 0; cc < SB; ++cc) {
+                const float4 l = *reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][4 * c4]);
+                acc[0] = fmaf(e8[cc], l.x, acc[0]);
+                acc[1] = fmaf(e8[cc], l.y, acc[1]);
+                acc[2] = fmaf(e8[cc], l.z, acc[2]);
+                acc[3] = fmaf(e8[cc], l.w, acc[3]);
+              }
+#pragma unroll
+              for (int y = 0; y < 4; ++y) sm.As[ab][4 * c4 + y][rr] = acc[y];
+            }
+            __syncwarp();
+            named_bar_arrive(BAR_X + (sp & 1), 128);  // sub-panel sp - 2 has all its in-panel feedback
+          }
+          TP_ACC(c_x, t4);
+          TP_T0(t5);
+          // the decision warp is past sub-panel sp: stage the next panel's weights there
+          if (hw == 2 && q + 1 < P) stage_w(jb - PW, SB * sp);
+          const int64_t j32 = jb + SB * sp;  // (when sp % 4 == 0) first column of a 32-group
+          if (hw == 0 && live && (sp & (32 / SB - 1)) == 0) {
+            const int g0 = SB * sp;
+            uint32_t pw[8];
 #pragma unroll
             for (int x = 0; x < 8; ++x)
-              if (jj + x >= 0) qd[x] = cv[x];
-          }
-        }
-        // a finished 64-column half of a source panel: per-row scale and int8 digits of E
-        // (the leftmost panel is never a source).  Lane sub quantizes columns
-        // [16 sub, 16 sub + 16) of the half; storage column = j + (npq - n), a multiple of 16.
-        const int64_t hs = npq - n + jb + 32 * sp;  // storage column of the half (sp even)
-        if ((sp & 1) == 0 && q < P - 1 && hs >= 0) {
-          float ev[16];
-          float mx = 0.0f;
+              pw[x] = sm.cs[g0 + 4 * x][rr] | (sm.cs[g0 + 4 * x + 1][rr] << 8) |
+                      (sm.cs[g0 + 4 * x + 2][rr] << 16) | ((uint32_t)sm.cs[g0 + 4 * x + 3][rr] << 24);
+            uint8_t* qd = Q + row * n + j32;
+            if (j32 >= 0 && (reinterpret_cast<uintptr_t>(qd) & 15) == 0) {
+              reinterpret_cast<uint4*>(qd)[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+              reinterpret_cast<uint4*>(qd)[1] = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+            } else {
 #pragma unroll
-          for (int x = 0; x < 16; ++x) {
-            ev[x] = sm.es[16 * sub + x][rr];
-            mx = fmaxf(mx, fabsf(ev[x]));
-          }
-          mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, 1));
-          mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, 2));
-          const float scale = (mx > 0.0f) ? mx / QSCALE : 0.0f;
-          const float inv = (mx > 0.0f) ? QSCALE / mx : 0.0f;
-          uint32_t dg[3][4];
-#pragma unroll
-          for (int x4 = 0; x4 < 4; ++x4) {
-            uint32_t w0 = 0, w1 = 0, w2 = 0;
-#pragma unroll
-            for (int y = 0; y < 4; ++y) {
-              int h = __float2int_rn(ev[4 * x4 + y] * inv);
-              const int d2 = ((h + 128) & 255) - 128;
-              h = (h - d2) >> 8;
-              const int d1 = ((h + 128) & 255) - 128;
-              const int d0 = (h - d1) >> 8;
-              w0 |= (uint32_t)(d0 & 255) << (8 * y);
-              w1 |= (uint32_t)(d1 & 255) << (8 * y);
-              w2 |= (uint32_t)(d2 & 255) << (8 * y);
+              for (int x = 0; x < 32; ++x)
+                if (j32 + x >= 0) qd[x] = (uint8_t)(pw[x >> 2] >> (8 * (x & 3)));
             }
-            dg[0][x4] = w0;
-            dg[1][x4] = w1;
-            dg[2][x4] = w2;
           }
-          if (live) {
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-              *reinterpret_cast<uint4*>(Eq + ((int64_t)d * m + row) * npq + hs + 16 * sub) =
-                  make_uint4(dg[d][0], dg[d][1], dg[d][2], dg[d][3]);
-            if (sub == 0) sE[(hs / UB) * mq + row] = scale;
-          }
-        }
-        TP_ACC(c_st, t4);
-        TP_T0(t5);
-        // feedback of this sub-panel into the sub-panels left of it: lane sub owns target
-        // columns [8 sub, 8 sub + 8) of every earlier sub-panel
+          // a finished 64-column half of a source panel (the leftmost panel is never one):
+          // per-row scale and three int8 digits of E (reading R-15); storage column
+          // hs = j + (npq - n), a multiple of 64
+          const int64_t hs = npq - n + j32;
+          if (hw == 1 && (sp & (64 / SB - 1)) == 0 && q < P - 1 && hs >= 0) {
+            const int g0 = SB * sp;
+            float mx = 0.0f;
+#pragma unroll 8
+            for (int x = 0; x < 64; ++x) mx = fmaxf(mx, fabsf(sm.es[g0 + x][rr]));
+            const float scale = (mx > 0.0f) ? mx / QSCALE : 0.0f;
+            const float inv = (mx > 0.0f) ? QSCALE / mx : 0.0f;
 #pragma unroll 1
-        for (int tp = 0; tp < sp; ++tp) {
-          float ac[8];
+            for (int x16 = 0; x16 < 4; ++x16) {
+              uint32_t dg[3][4];
 #pragma unroll
-          for (int x = 0; x < 8; ++x) ac[x] = sm.As[ab][32 * tp + 8 * sub + x][rr];
-#pragma unroll 4
-          for (int cc = 0; cc < 32; ++cc) {
-            const float ec = esp[cc][rr];
-            const float4* lrow = reinterpret_cast<const float4*>(&sm.Ld[32 * sp + cc][32 * tp + 8 * sub]);
-            const float4 l0 = lrow[0], l1 = lrow[1];
-            ac[0] = fmaf(ec, l0.x, ac[0]);
-            ac[1] = fmaf(ec, l0.y, ac[1]);
-            ac[2] = fmaf(ec, l0.z, ac[2]);
-            ac[3] = fmaf(ec, l0.w, ac[3]);
-            ac[4] = fmaf(ec, l1.x, ac[4]);
-            ac[5] = fmaf(ec, l1.y, ac[5]);
-            ac[6] = fmaf(ec, l1.z, ac[6]);
-            ac[7] = fmaf(ec, l1.w, ac[7]);
+              for (int x4 = 0; x4 < 4; ++x4) {
+                uint32_t w0 = 0, w1 = 0, w2 = 0;
+#pragma unroll
+                for (int y = 0; y < 4; ++y) {
+                  int h = __float2int_rn(sm.es[g0 + 16 * x16 + 4 * x4 + y][rr] * inv);
+                  const int d2 = ((h + 128) & 255) - 128;
+                  h = (h - d2) >> 8;
+                  const int d1 = ((h + 128) & 255) - 128;
+                  const int d0 = (h - d1) >> 8;
+                  w0 |= (uint32_t)(d0 & 255) << (8 * y);
+                  w1 |= (uint32_t)(d1 & 255) << (8 * y);
+                  w2 |= (uint32_t)(d2 & 255) << (8 * y);
+                }
+                dg[0][x4] = w0;
+                dg[1][x4] = w1;
+                dg[2][x4] = w2;
+              }
+              if (live) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d)
+                  *reinterpret_cast<uint4*>(Eq + ((int64_t)d * m + row) * npq + hs + 16 * x16) =
+                      make_uint4(dg[d][0], dg[d][1], dg[d][2], dg[d][3]);
+              }
+            }
+            if (live) sE[(hs / UB) * mq + row] = scale;
+            sm.sEn[sp / (64 / SB)][rr] = scale;  // half 0 / 1 of this panel, for the readers
           }
-#pragma unroll
-          for (int x = 0; x < 8; ++x) sm.As[ab][32 * tp + 8 * sub + x][rr] = ac[x];
+          TP_ACC(c_st, t5);
         }
-        TP_ACC(c_x, t5);
-        TP_T0(t6);
-        named_bar_sync(pbar, 128);  // As updated, es / cs free for the next sub-panel
-        TP_ACC(c_bar, t6);
+        asm volatile("cp.async.wait_all;" ::: "memory");  // the next panel's weights are in ws
+        fence_proxy_async_global();  // residual digit stores -> visible to the TMA (async proxy)
+        named_bar_sync(BAR_PANEL, 128);
+        if (warp == 7 && lane == 0) {
+          mbar_arrive(&sm.ebar);
+          mbar_arrive(&sm.as_free[ab]);
+        }
       }
-      fence_proxy_async_global();  // residual digit stores -> visible to the TMA (async proxy)
-      named_bar_sync(pbar, 128);
-      if (pl == 0) {
-        mbar_arrive(&sm.ebar);
-        mbar_arrive(&sm.as_free[ab]);
-      }
+      long long tot = 0;
+      TP_ACC(tot, t_all);
+      tp_flush(dbg, lane, 13, c_st);
+      tp_flush(dbg, lane, 14, c_x);
+      (void)tot;
     }
-    long long tot = 0;
-    TP_ACC(tot, t_all);
-    tp_flush(dbg, lane, 9, tot);
-    tp_flush(dbg, lane, 10, w_acc);
-    tp_flush(dbg, lane, 11, w_ld);
-    tp_flush(dbg, lane, 12, c_dec);
-    tp_flush(dbg, lane, 13, c_st);
-    tp_flush(dbg, lane, 14, c_x);
-    tp_flush(dbg, lane, 15, c_bar);
   }
   tc_fence_before();
   __syncthreads();
@@ -642,11 +751,11 @@ ganq_status_t launch_t(const float* W, const float* Lhat, const int8_t* LTq, con
     const double c = (double)((groups + CS - 1) / CS * CS);
     fprintf(stderr,
             "ssprof per CTA (kcyc): tma %.1f (empty %.1f, ebar %.1f) | mma %.1f (tempty %.1f, full %.1f) | "
-            "rd/warp %.1f (tfull %.1f, as_free %.1f) | panel/warp %.1f (acc_ready %.1f, ld %.1f, dec %.1f, "
-            "st %.1f, cross %.1f, bar %.1f)\n",
+            "rd/warp %.1f (tfull %.1f, as_free %.1f) | decide %.1f (acc_ready %.1f, ld %.1f, dec %.1f, "
+            "bar %.1f) | helper/warp st %.1f, cross %.1f\n",
             h[0] / c / 1e3, h[1] / c / 1e3, h[2] / c / 1e3, h[3] / c / 1e3, h[4] / c / 1e3, h[5] / c / 1e3,
-            h[6] / c / 4e3, h[7] / c / 4e3, h[8] / c / 4e3, h[9] / c / 4e3, h[10] / c / 4e3, h[11] / c / 4e3,
-            h[12] / c / 4e3, h[13] / c / 4e3, h[14] / c / 4e3, h[15] / c / 4e3);
+            h[6] / c / 4e3, h[7] / c / 4e3, h[8] / c / 4e3, h[9] / c / 1e3, h[10] / c / 1e3, h[11] / c / 1e3,
+            h[12] / c / 1e3, h[15] / c / 1e3, h[13] / c / 3e3, h[14] / c / 3e3);
     const unsigned long long z[16] = {};
     cudaMemcpyToSymbol(g_ssprof, z, sizeof(z));
   }
