@@ -19,6 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]
+if os.environ.get("GANQ_KPROF") == "1":  # per-warp-role cycle accounting (tools/*_prof.sh only)
+    FLAGS.append("-DGANQ_KPROF")
 
 
 def sources():

@@ -254,6 +254,12 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// shared memory -> TMEM copy of a 128-row x 32-byte matrix (smem descriptor as for an MMA
+// operand) into 8 consecutive TMEM columns of lanes 0-127; ordered with the issuing thread's
+// later tcgen05.mma like any tcgen05 operation of the same thread.
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 // CTA-pair (cta_group::2) variants: issued by the leader CTA; A rows 0-127 / 128-255 and the
 // two N halves of B live at the same TMEM / shared offsets of the two CTAs.
 __device__ __forceinline__ void mma_i8_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,

@@ -12,7 +12,8 @@
 // computed in exact integer arithmetic on tcgen05.mma kind::i8 (reading R-15): per 64-u block
 // both operands are 24-bit fixed point with their own scale (LhatT per (column, block), E per
 // (row, block)), split into three balanced int8 digits; the six digit products of weight
-// >= 2^16 go to three int32 TMEM accumulators (weights 2^32, 2^24, 2^16), exact in any order.  The
+// >= 2^16 are exact int32 sums: one MMA per LhatT digit against the stacked E digits (N = 96,
+// 64, 32), offset so that equal weights (2^32, 2^24, 2^16) accumulate in the same columns.  The
 // reader warps scale each block's integer sums and add them in fp32 registers.  Blocks are
 // issued oldest first, so the feedback of panel q-1 runs while panel q is still being decided;
 // only its last 2 blocks wait for panel q's residuals.  The panel group makes the 128
@@ -40,7 +41,7 @@ constexpr int SB = 8;               // decision sub-panel width
 constexpr int NSUB = PW / SB;
 constexpr int UB = 64;              // u per feedback block (64-byte SW64 rows of int8 digits)
 constexpr int STAGES = 3;
-constexpr int NBUF = 4;             // TMEM accumulator sets of 3 x 32 columns (weights 2^16, 2^8, 1)
+constexpr int NBUF = 4;             // TMEM accumulator sets of 3 x 32 columns (weight groups)
 constexpr int BUF_COLS = 3 * RB;
 constexpr int CS = 4;               // cluster size: row groups sharing each LhatT tile (multicast)
 constexpr uint16_t CMASK = (1u << CS) - 1u;
@@ -48,14 +49,9 @@ constexpr int A_TILE = PW * UB;     // 8 KB: one digit of LhatT (128 panel colum
 constexpr int B_TILE = RB * UB;     // 2 KB: one digit of E (32 rows x 64 u)
 constexpr int STAGE_BYTES = 3 * A_TILE + 3 * B_TILE;  // 30 KB
 constexpr int THREADS = 320;   // 10 warps: TMA, MMA, 4 readers, 4 panel
-constexpr uint32_t IDESC = umma_idesc_s8(PW, RB);
+// digit a of LhatT times the E digits b = 0 .. 2 - a: N = 32 (3 - a)
+__host__ __device__ constexpr uint32_t idesc_digit(int a) { return umma_idesc_s8(PW, RB * (3 - a)); }
 constexpr float QSCALE = 8388608.0f - 65536.0f;  // 2^23 - 2^16: |fixed-point value| bound
-// digit products (a = LhatT digit, b = E digit, weight group 2 - (a + b)); digit 0 is the top
-constexpr int NPROD = 6;
-__host__ __device__ constexpr int prod_a(int p) { return p == 0 ? 0 : p == 1 ? 0 : p == 2 ? 1 : p == 3 ? 0 : p == 4 ? 1 : 2; }
-__host__ __device__ constexpr int prod_b(int p) { return p == 0 ? 0 : p == 1 ? 1 : p == 2 ? 0 : p == 3 ? 2 : p == 4 ? 1 : 0; }
-__host__ __device__ constexpr bool prod_first(int p) { return p == 0 || p == 1 || p == 3; }
-
 struct SsSmem {
   alignas(128) float Ld[PW][PW];         // Lhat[jb + c][jb + c2] of the current panel (TMA)
   alignas(16) float As[2][PW][RB + 1];   // drained feedback per (panel column, row), 2 buffers
@@ -224,15 +220,17 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             tc_fence_after();
             const uint32_t st = smem_u32(tiles + s * STAGE_BYTES);
             const uint32_t d = tmem + buf * BUF_COLS;
+            // one MMA per LhatT digit a against the stacked E digits [b0; b1; ...; b_{2-a}]
+            // (N = 32 (3 - a)) written from column 32 a, so that product (a, b) lands in column
+            // range a + b: the tensor core adds equal weights (2^32, 2^24, 2^16) in exact int32,
+            // and streams each A tile once per K step
 #pragma unroll
-            for (int p = 0; p < NPROD; ++p) {
-              const int wgt = 2 - (prod_a(p) + prod_b(p));  // 2 -> 2^16, 1 -> 2^8, 0 -> 1
-              const uint32_t a = st + prod_a(p) * A_TILE, b = st + 3 * A_TILE + prod_b(p) * B_TILE;
+            for (int kk = 0; kk < UB / 32; ++kk)
 #pragma unroll
-              for (int kk = 0; kk < UB / 32; ++kk)
-                mma_i8(d + (2 - wgt) * RB, umma_desc_sw64(a + kk * 32), umma_desc_sw64(b + kk * 32), IDESC,
-                       (prod_first(p) && kk == 0) ? 0u : 1u);
-            }
+              for (int dg = 0; dg < 3; ++dg)
+                mma_i8(d + dg * RB, umma_desc_sw64(st + dg * A_TILE + kk * 32),
+                       umma_desc_sw64(st + 3 * A_TILE + kk * 32), idesc_digit(dg),
+                       (kk == 0 && dg == 0) ? 0u : 1u);
             mma_commit_mc(&sm.empty[s], CMASK);  // frees stage s in every CTA of the cluster
             mma_commit(&sm.tfull[buf]);
           }
@@ -254,29 +252,41 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       float acc[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) acc[r] = 0.0f;
-      for (int qs = 0; qs < q; ++qs) {
-        for (int k2 = 0; k2 < PW / UB; ++k2, ++kb) {
-          const uint32_t buf = kb % NBUF;
-          const int64_t blk = (npq - (int64_t)PW * (qs + 1)) / UB + k2;  // storage block of u
-          // block scales: LhatT per (column, block), E per (row, block); the digit weights of the
-          // three groups are 2^32, 2^24, 2^16 = 2^16 x (65536, 256, 1).  Scales of older source
-          // panels are read before the wait; those of the newest one (qs = q - 1) come from the
-          // panel group's shared copy after tfull (ordered after its stores by ebar -> TMA ->
-          // MMA -> commit).
-          const float tl = (j >= 0) ? __ldg(tL + blk * n + j) * 65536.0f : 0.0f;
-          float se[RB];
-          const bool newest = (qs == q - 1);
-          if (!newest) {
-            const float4* sp4 = reinterpret_cast<const float4*>(sE + blk * ((m + RB - 1) / RB * RB) + r0);
+      // block scales: LhatT per (column, block), E per (row, block); the digit weights of the
+      // three groups are 2^32, 2^24, 2^16 = 2^16 x (65536, 256, 1).  Scales of older source panels
+      // are loaded one block ahead (the readers may run behind the MMA, so a load issued right
+      // before its tfull wait would not be hidden); those of the newest source panel (qs = q - 1)
+      // come from the panel group's shared copy after tfull (ordered after its stores by ebar ->
+      // TMA -> MMA -> commit).
+      const int nblkq = q * (PW / UB);
+      auto load_scales = [&](int i, float& tl_o, float (&se_o)[RB]) {
+        const int qs = i / (PW / UB), k2 = i % (PW / UB);
+        const int64_t blk = (npq - (int64_t)PW * (qs + 1)) / UB + k2;  // storage block of u
+        tl_o = __ldg(tL + blk * n + (j >= 0 ? j : 0));  // raw: consumed a block later
+        if (qs != q - 1) {
+          const float4* sp4 = reinterpret_cast<const float4*>(sE + blk * ((m + RB - 1) / RB * RB) + r0);
 #pragma unroll
-            for (int r4 = 0; r4 < RB / 4; ++r4) {
-              const float4 v4 = sp4[r4];
-              se[4 * r4 + 0] = v4.x;
-              se[4 * r4 + 1] = v4.y;
-              se[4 * r4 + 2] = v4.z;
-              se[4 * r4 + 3] = v4.w;
-            }
+          for (int r4 = 0; r4 < RB / 4; ++r4) {
+            const float4 v4 = sp4[r4];
+            se_o[4 * r4 + 0] = v4.x;
+            se_o[4 * r4 + 1] = v4.y;
+            se_o[4 * r4 + 2] = v4.z;
+            se_o[4 * r4 + 3] = v4.w;
           }
+        }
+      };
+      float tl_n = 0.0f, se_n[RB];
+      if (nblkq > 0) load_scales(0, tl_n, se_n);
+      for (int i = 0; i < nblkq; ++i, ++kb) {
+        {
+          const uint32_t buf = kb % NBUF;
+          const int k2 = i % (PW / UB);
+          const bool newest = (i / (PW / UB) == q - 1);
+          const float tl = tl_n;
+          float se[RB];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) se[r] = se_n[r];
+          if (i + 1 < nblkq) load_scales(i + 1, tl_n, se_n);
           TP_T0(t0);
           mbar_wait(&sm.tfull[buf], (kb / NBUF) & 1);
           TP_ACC(w_tf, t0);
@@ -285,8 +295,9 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
 #pragma unroll
             for (int r = 0; r < RB; ++r) se[r] = sm.sEn[k2][r];
           }
+          const float tls = (j >= 0) ? tl * 65536.0f : 0.0f;
 #pragma unroll
-          for (int r = 0; r < RB; ++r) se[r] *= tl;
+          for (int r = 0; r < RB; ++r) se[r] *= tls;
           const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BUF_COLS;
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {  // rows [16 hh, 16 hh + 16): three weight groups

@@ -50,10 +50,16 @@ constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile 
 constexpr uint32_t IDESC = umma_idesc_u8s8(128, TJ);  // A = one-hot bytes 0 / 128 (u8)
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
 
-// debug-only cycle accounting per warp role (GANQ_TGRAM_DBG & 16)
+// debug-only cycle accounting per warp role: compiled with -DGANQ_KPROF, enabled at run time
+// by GANQ_TGRAM_DBG & 16 (tools/tg_prof.sh); absent from the default build
 __device__ unsigned long long g_tgprof[16];
+#ifdef GANQ_KPROF
 #define TP_T0(v) long long v = (dbg & 16) ? clock64() : 0
 #define TP_ACC(acc, v) do { if (dbg & 16) acc += clock64() - v; } while (0)
+#else
+#define TP_T0(v) constexpr long long v = 0
+#define TP_ACC(acc, v) do { (void)(acc); (void)(v); } while (0)
+#endif
 __device__ __forceinline__ void tp_flush(int dbg, int lane, int slot, long long v) {
   if ((dbg & 16) && lane == 0) atomicAdd(&g_tgprof[slot], (unsigned long long)v);
 }

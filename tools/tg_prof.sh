@@ -1,3 +1,5 @@
 #!/bin/bash
-# per-role cycle accounting of tgram_tc (debug only), one bench step
-GANQ_TGRAM_DBG=${1:-16} timeout 200 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 >/dev/null | grep tgprof | tail -3
+# per-role cycle accounting of tgram_tc (debug build with -DGANQ_KPROF), one bench step
+GANQ_KPROF=1 python -c "from paper_2501_12956_b200 import build as b; b.build(force=True)" >/dev/null 2>&1
+GANQ_TGRAM_DBG=${1:-16} timeout -s KILL 200 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 >/dev/null | grep tgprof | tail -1
+python -c "from paper_2501_12956_b200 import build as b; b.build(force=True)" >/dev/null 2>&1
