@@ -21,7 +21,7 @@
 // finished 64-column half of residuals for the tensor cores.
 //
 // Warps: 0 = TMA producer, 1 = MMA issuer (+TMEM owner), 2-5 = TMEM readers (one lane
-// quarter each), 6 = decisions (lane = row), 7-9 = in-panel feedback, code and digit stores.
+// quarter each), 6 = decisions (lane = row), 7-11 = in-panel feedback, code and digit stores.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -48,7 +48,9 @@ constexpr uint16_t CMASK = (1u << CS) - 1u;
 constexpr int A_TILE = PW * UB;     // 8 KB: one digit of LhatT (128 panel columns x 64 u)
 constexpr int B_TILE = RB * UB;     // 2 KB: one digit of E (32 rows x 64 u)
 constexpr int STAGE_BYTES = 3 * A_TILE + 3 * B_TILE;  // 30 KB
-constexpr int THREADS = 320;   // 10 warps: TMA, MMA, 4 readers, 4 panel
+constexpr int NHELP = 3;        // in-panel helper warps
+constexpr int THREADS = 32 * (7 + NHELP);  // TMA, MMA, 4 readers, decisions, helpers
+constexpr int PANEL_THREADS = 32 * (1 + NHELP);
 // digit a of LhatT times the E digits b = 0 .. 2 - a: N = 32 (3 - a)
 __host__ __device__ constexpr uint32_t idesc_digit(int a) { return umma_idesc_s8(PW, RB * (3 - a)); }
 constexpr float QSCALE = 8388608.0f - 65536.0f;  // 2^23 - 2^16: |fixed-point value| bound
@@ -334,7 +336,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     tp_flush(dbg, lane, 7, w_tf);
     tp_flush(dbg, lane, 8, w_af);
   } else {
-    // ---------------- panel group (warps 6-9).  Warp 6 decides (lane = row); warps 7-9 apply
+    // ---------------- panel group (warps 6-11).  Warp 6 decides (lane = row); warps 7-11 apply
     // the feedback between sub-panels (the next sub-panel's first, handed over by a named
     // barrier), store the codes and quantize finished halves of residuals for the tensor cores.
     const int64_t mq = (m + RB - 1) / RB * RB;  // rows of the sE table
@@ -392,7 +394,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           above = th[s2];
         }
       }
-      named_bar_sync(BAR_PANEL, 128);  // the helpers staged panel 0's weights
+      named_bar_sync(BAR_PANEL, PANEL_THREADS);  // the helpers staged panel 0's weights
       TP_T0(t_all);
       long long w_acc = 0, w_ld = 0, c_dec = 0, c_bar = 0;
       for (int q = 0; q < P; ++q) {
@@ -410,11 +412,13 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           const int64_t j0 = jb + SB * sp;  // first column of the sub-panel (may be < 0)
           TP_T0(tb);
           // the helpers' feedback from sub-panels >= sp + 2 into sp (none for the first two)
-          if (sp < NSUB - 2) named_bar_sync(BAR_X + (sp & 1), 128);
+          if (sp < NSUB - 2) named_bar_sync(BAR_X + (sp & 1), PANEL_THREADS);
           TP_ACC(c_bar, tb);
           TP_T0(t2);
-          float a[SB], w[SB], ev[SB];
+          float a[SB], w[SB], ev[SB], lc[SB];
           int iv[SB];
+#pragma unroll
+          for (int cc = 1; cc < SB; ++cc) lc[cc] = sm.Ld[SB * sp + cc][SB * sp + cc - 1];  // critical path
 #pragma unroll
           for (int k = 0; k < SB; ++k) {
             a[k] = sm.As[ab][SB * sp + k][lane];
@@ -433,16 +437,18 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             const float ec = (j0 + cc >= 0) ? __fsub_rn(w[cc], tq) : 0.0f;
             ev[cc] = ec;  // stored after the sub-panel: no shared stores between the Ld loads
             iv[cc] = iq;
-            // in-sub-panel feedback into the columns left of cc (entries >= cc are already used)
+            // in-sub-panel feedback into the columns left of cc (entries >= cc are already used);
+            // the coefficient of column cc - 1 (the next decision) comes from a register
+            if (cc > 0) a[cc - 1] = fmaf(ec, lc[cc], a[cc - 1]);
             const float4* lrow = reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][SB * sp]);
 #pragma unroll
             for (int k4 = 0; k4 < SB / 4; ++k4) {
-              if (4 * k4 < cc) {
+              if (4 * k4 < cc - 1) {
                 const float4 l = lrow[k4];
-                a[4 * k4 + 0] = fmaf(ec, l.x, a[4 * k4 + 0]);
-                a[4 * k4 + 1] = fmaf(ec, l.y, a[4 * k4 + 1]);
-                a[4 * k4 + 2] = fmaf(ec, l.z, a[4 * k4 + 2]);
-                a[4 * k4 + 3] = fmaf(ec, l.w, a[4 * k4 + 3]);
+                if (4 * k4 + 0 < cc - 1) a[4 * k4 + 0] = fmaf(ec, l.x, a[4 * k4 + 0]);
+                if (4 * k4 + 1 < cc - 1) a[4 * k4 + 1] = fmaf(ec, l.y, a[4 * k4 + 1]);
+                if (4 * k4 + 2 < cc - 1) a[4 * k4 + 2] = fmaf(ec, l.z, a[4 * k4 + 2]);
+                if (4 * k4 + 3 < cc - 1) a[4 * k4 + 3] = fmaf(ec, l.w, a[4 * k4 + 3]);
               }
             }
             // ... and into the next sub-panel
@@ -465,10 +471,10 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           }
           TP_ACC(c_dec, t2);
           __syncwarp();
-          named_bar_arrive(BAR_ES + (sp & 1), 128);  // es / cs of sub-panel sp are complete
+          named_bar_arrive(BAR_ES + (sp & 1), PANEL_THREADS);  // es / cs of sub-panel sp are complete
         }
         TP_T0(t3);
-        named_bar_sync(BAR_PANEL, 128);  // the helpers finished the panel
+        named_bar_sync(BAR_PANEL, PANEL_THREADS);  // the helpers finished the panel
         TP_ACC(c_bar, t3);
       }
       long long tot = 0;
@@ -500,9 +506,9 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             sm.ws[c0 + k][rr] = 0.0f;
         }
       };
-      for (int c0 = hw * SB; c0 < PW; c0 += 3 * SB) stage_w(n - PW, c0);
+      for (int c0 = hw * SB; c0 < PW; c0 += NHELP * SB) stage_w(n - PW, c0);
       asm volatile("cp.async.wait_all;" ::: "memory");
-      named_bar_sync(BAR_PANEL, 128);
+      named_bar_sync(BAR_PANEL, PANEL_THREADS);
       TP_T0(t_all);
       long long c_x = 0, c_st = 0;
       for (int q = 0; q < P; ++q) {
@@ -512,7 +518,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         mbar_wait(&sm.ldbar, q & 1);
 #pragma unroll 1
         for (int sp = NSUB - 1; sp >= 0; --sp) {
-          named_bar_sync(BAR_ES + (sp & 1), 128);  // the decision warp finished sub-panel sp
+          named_bar_sync(BAR_ES + (sp & 1), PANEL_THREADS);  // the decision warp finished sub-panel sp
           TP_T0(t4);
           if (sp >= 2) {
             float e8[SB];
@@ -520,7 +526,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             for (int cc = 0; cc < SB; ++cc) e8[cc] = sm.es[SB * sp + cc][rr];
             const int nch = SB * (sp - 1) / 4;  // 4-column chunks of the columns [0, SB (sp - 1))
 #pragma unroll 1
-            for (int c4 = hw; c4 < nch; c4 += 3) {
+            for (int c4 = hw; c4 < nch; c4 += NHELP) {
               float acc[4];
 #pragma unroll
               for (int y = 0; y < 4; ++y) acc[y] = sm.As[ab][4 * c4 + y][rr];
@@ -536,7 +542,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
               for (int y = 0; y < 4; ++y) sm.As[ab][4 * c4 + y][rr] = acc[y];
             }
             __syncwarp();
-            named_bar_arrive(BAR_X + (sp & 1), 128);  // sub-panel sp - 2 has all its in-panel feedback
+            named_bar_arrive(BAR_X + (sp & 1), PANEL_THREADS);  // sub-panel sp - 2 has all its in-panel feedback
           }
           TP_ACC(c_x, t4);
           TP_T0(t5);
@@ -606,7 +612,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         }
         asm volatile("cp.async.wait_all;" ::: "memory");  // the next panel's weights are in ws
         fence_proxy_async_global();  // residual digit stores -> visible to the TMA (async proxy)
-        named_bar_sync(BAR_PANEL, 128);
+        named_bar_sync(BAR_PANEL, PANEL_THREADS);
         if (warp == 7 && lane == 0) {
           mbar_arrive(&sm.ebar);
           mbar_arrive(&sm.as_free[ab]);
