@@ -79,7 +79,7 @@ struct StageScope {
 namespace {
 
 struct Layout {
-  size_t A64, Lhat, LTq, tL, Eq, sE, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, Xhi, Xlo, Hhi,
+  size_t A64, Lhat, LTq, tL, Eq, sE, hdiag, H32, WH, E, EH, G, Dv, b, cnt, fb, Hq, qscale, Xhi, Xlo, Hhi,
       Hlo, status, mean, per_row, total_d, end;
 };
 
@@ -100,6 +100,7 @@ Layout make_layout(int64_t m, int64_t n, int nlev) {
   L.tL = take(nblk * (size_t)n * sizeof(float));   // their per (block, column) scales
   L.Eq = take(3 * (size_t)m * npq);                // int8 digits of the residuals E
   L.sE = take(nblk * mq * sizeof(float));          // their per (block, row) scales
+  L.hdiag = take((size_t)n * sizeof(double));      // H_jj (T-update right-hand side)
   L.H32 = take(nn * sizeof(float));
   L.WH = take(mn * sizeof(float));
   L.E = take(mn * sizeof(float));
@@ -323,6 +324,7 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
   {
     GANQ_STAGE(ST_DERIVE);
     if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
+    if ((s = launch_hdiag(H, n, at<double>(ws, L.hdiag), st))) return s;
     if ((s = launch_lhat_prep(at<double>(ws, L.A64), n, Lhat, at<int8_t>(ws, L.LTq), at<float>(ws, L.tL), st)))
       return s;
     // block scales of rows >= m are never written but are read (multiplied by zero digits)
@@ -371,7 +373,7 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
           return s;
       }
       GANQ_STAGE(ST_TSOLVE);
-      if ((s = launch_tsolve(H, WH, Q, m, n, nlev, o.empty_level_rule, T, at<double>(ws, L.G),
+      if ((s = launch_tsolve(at<double>(ws, L.hdiag), WH, Q, m, n, nlev, o.empty_level_rule, T, at<double>(ws, L.G),
                              at<double>(ws, L.Dv), at<double>(ws, L.b), at<int>(ws, L.cnt), at<int>(ws, L.fb),
                              st)))
         return s;
@@ -487,7 +489,8 @@ ganq_status_t ganq_tstep(const float* W, const uint8_t* Q, const double* H, int6
   if ((s = launch_tgram_tc(at<int8_t>(workspace, L.Hq), at<double>(workspace, L.qscale), Q, m, n, nlev,
                            at<double>(workspace, L.G), st)))
     return s;
-  return launch_tsolve(H, WH, Q, m, n, nlev, empty_level_rule, T, at<double>(workspace, L.G),
+  if ((s = launch_hdiag(H, n, at<double>(workspace, L.hdiag), st))) return s;
+  return launch_tsolve(at<double>(workspace, L.hdiag), WH, Q, m, n, nlev, empty_level_rule, T, at<double>(workspace, L.G),
                        at<double>(workspace, L.Dv), at<double>(workspace, L.b), at<int>(workspace, L.cnt),
                        at<int>(workspace, L.fb), st);
 }

@@ -44,7 +44,8 @@ ganq_status_t launch_derive_operands(const double* L, const double* H, int64_t n
 ganq_status_t launch_init_codebook(const float* W, int64_t m, int64_t n, int nlev, float* T,
                                    cudaStream_t st);
 // the T-update after the normal matrices (launch_tgram_tc): right-hand sides and the solves
-ganq_status_t launch_tsolve(const double* H, const float* WH, const uint8_t* Q, int64_t m, int64_t n, int nlev,
+ganq_status_t launch_hdiag(const double* H, int64_t n, double* hdiag, cudaStream_t st);  // H_jj, once per layer
+ganq_status_t launch_tsolve(const double* hdiag, const float* WH, const uint8_t* Q, int64_t m, int64_t n, int nlev,
                             int empty_rule, float* T, double* G, double* Dv, double* b, int* cnt, int* fallback,
                             cudaStream_t st);
 // tgram_tc.cu

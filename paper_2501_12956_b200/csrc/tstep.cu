@@ -19,49 +19,78 @@ namespace {
 constexpr int kTgramSplit = 4;  // == SPLIT in tgram_tc.cu
 
 // Per row (one warp): D_i[a] = sum_j [q_ij=a] H_jj, b_i[a] = sum_j [q_ij=a] (W H)_ij and the
-// level counts (fp64 accumulation; lanes over j, warp-shuffle reduction in fixed order).
+// level counts.  Lane l accumulates the columns j = l (mod 32) into its own shared slots
+// [level][lane] (no atomics, no per-level selects); the 32 lane partials of each level are then
+// added in a fixed order (fp64), so the sums are deterministic.
+constexpr int TRHS_WARPS = 4;
 template <int NLEV>
-__global__ void __launch_bounds__(256)
-trhs_kernel(const double* __restrict__ H, const float* __restrict__ WH, const uint8_t* __restrict__ Q,
-            int64_t m, int64_t n, double* __restrict__ Dv, double* __restrict__ bvec,
-            int* __restrict__ cnt) {
+__global__ void __launch_bounds__(32 * TRHS_WARPS)
+trhs_kernel(const double* __restrict__ hdiag, const float* __restrict__ WH, const uint8_t* __restrict__ Q,
+            int64_t m, int64_t n, double* __restrict__ Dv, double* __restrict__ bvec, int* __restrict__ cnt) {
+  __shared__ double sD[TRHS_WARPS][NLEV][32], sR[TRHS_WARPS][NLEV][32];
+  __shared__ int sC[TRHS_WARPS][NLEV][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t row = (int64_t)blockIdx.x * TRHS_WARPS + warp;
   if (row >= m) return;
-  const uint8_t* q = Q + row * n;
-  const float* wh = WH + row * n;
-  double dsum[NLEV], rsum[NLEV];
-  int c[NLEV];
-#pragma unroll
-  for (int a = 0; a < NLEV; ++a) { dsum[a] = 0.0; rsum[a] = 0.0; c[a] = 0; }
-  for (int64_t j = lane; j < n; j += 32) {
-    const int qj = q[j];
-    const double hd = H[j * n + j];
-    const double r = (double)wh[j];
-#pragma unroll
-    for (int a = 0; a < NLEV; ++a) {
-      const bool hit = qj == a;
-      dsum[a] += hit ? hd : 0.0;
-      rsum[a] += hit ? r : 0.0;
-      c[a] += hit ? 1 : 0;
-    }
-  }
 #pragma unroll
   for (int a = 0; a < NLEV; ++a) {
-    for (int o = 16; o; o >>= 1) {
-      dsum[a] += __shfl_xor_sync(0xffffffffu, dsum[a], o);
-      rsum[a] += __shfl_xor_sync(0xffffffffu, rsum[a], o);
-      c[a] += __shfl_xor_sync(0xffffffffu, c[a], o);
-    }
+    sD[warp][a][lane] = 0.0;
+    sR[warp][a][lane] = 0.0;
+    sC[warp][a][lane] = 0;
   }
-  if (lane == 0) {
+  __syncwarp();
+  const uint8_t* q = Q + row * n;
+  const float* wh = WH + row * n;
+  auto add = [&](int a, double hd, float r) {
+    if (a < NLEV) {  // codes >= 2^N (only possible through ganq_tstep) belong to no level
+      sD[warp][a][lane] += hd;
+      sR[warp][a][lane] += (double)r;
+      sC[warp][a][lane] += 1;
+    }
+  };
+  int64_t j0 = 0;
+  if ((n & 3) == 0) {
+    // lane takes 4 consecutive columns per 128-column step; two steps of loads in flight
+    for (; j0 + 256 <= n; j0 += 256) {
+      uint32_t qv[2];
+      float4 wv[2];
+      double2 h0[2], h1[2];
 #pragma unroll
-    for (int a = 0; a < NLEV; ++a) {
-      Dv[row * NLEV + a] = dsum[a];
-      bvec[row * NLEV + a] = rsum[a];
-      cnt[row * NLEV + a] = c[a];
+      for (int u = 0; u < 2; ++u) {
+        const int64_t j = j0 + 128 * u + 4 * lane;
+        qv[u] = *reinterpret_cast<const uint32_t*>(q + j);
+        wv[u] = *reinterpret_cast<const float4*>(wh + j);
+        h0[u] = *reinterpret_cast<const double2*>(hdiag + j);
+        h1[u] = *reinterpret_cast<const double2*>(hdiag + j + 2);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        add(qv[u] & 255, h0[u].x, wv[u].x);
+        add((qv[u] >> 8) & 255, h0[u].y, wv[u].y);
+        add((qv[u] >> 16) & 255, h1[u].x, wv[u].z);
+        add(qv[u] >> 24, h1[u].y, wv[u].w);
+      }
     }
   }
+  for (int64_t j = j0 + lane; j < n; j += 32) add(q[j], hdiag[j], wh[j]);
+  __syncwarp();
+  if (lane < NLEV) {
+    double d = 0.0, r = 0.0;
+    int c = 0;
+    for (int l = 0; l < 32; ++l) {
+      d += sD[warp][lane][l];
+      r += sR[warp][lane][l];
+      c += sC[warp][lane][l];
+    }
+    Dv[row * NLEV + lane] = d;
+    bvec[row * NLEV + lane] = r;
+    cnt[row * NLEV + lane] = c;
+  }
+}
+
+__global__ void hdiag_kernel(const double* __restrict__ H, int64_t n, double* __restrict__ hdiag) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) hdiag[j] = H[j * n + j];
 }
 
 // One warp per row; lane l < NLEV holds row l of the (regularised) system.
@@ -242,10 +271,11 @@ __global__ void init_codebook_kernel(const float* __restrict__ W, int64_t m, int
 }
 
 template <int NLEV>
-ganq_status_t launch_tsolve_t(const double* H, const float* WH, const uint8_t* Q, int64_t m, int64_t n,
+ganq_status_t launch_tsolve_t(const double* hdiag, const float* WH, const uint8_t* Q, int64_t m, int64_t n,
                               int empty_rule, float* T, double* G, double* Dv, double* b, int* cnt, int* fb,
                               cudaStream_t st) {
-  trhs_kernel<NLEV><<<(unsigned)((m + 7) / 8), 256, 0, st>>>(H, WH, Q, m, n, Dv, b, cnt);
+  trhs_kernel<NLEV><<<(unsigned)((m + TRHS_WARPS - 1) / TRHS_WARPS), 32 * TRHS_WARPS, 0, st>>>(hdiag, WH, Q, m, n,
+                                                                                               Dv, b, cnt);
   GANQ_LAUNCH_CHECK("trhs_kernel");
   tsolve_kernel<NLEV><<<(unsigned)((m + 7) / 8), 256, 0, st>>>(G, Dv, b, cnt, m, empty_rule, T, fb);
   GANQ_LAUNCH_CHECK("tsolve_kernel");
@@ -264,14 +294,20 @@ ganq_status_t launch_init_codebook(const float* W, int64_t m, int64_t n, int nle
   return GANQ_OK;
 }
 
-ganq_status_t launch_tsolve(const double* H, const float* WH, const uint8_t* Q, int64_t m, int64_t n, int nlev,
+ganq_status_t launch_hdiag(const double* H, int64_t n, double* hdiag, cudaStream_t st) {
+  hdiag_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(H, n, hdiag);
+  GANQ_LAUNCH_CHECK("hdiag_kernel");
+  return GANQ_OK;
+}
+
+ganq_status_t launch_tsolve(const double* hdiag, const float* WH, const uint8_t* Q, int64_t m, int64_t n, int nlev,
                             int empty_rule, float* T, double* G, double* Dv, double* b, int* cnt, int* fb,
                             cudaStream_t st) {
   switch (nlev) {
-    case 2: return launch_tsolve_t<2>(H, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
-    case 4: return launch_tsolve_t<4>(H, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
-    case 8: return launch_tsolve_t<8>(H, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
-    case 16: return launch_tsolve_t<16>(H, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 2: return launch_tsolve_t<2>(hdiag, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 4: return launch_tsolve_t<4>(hdiag, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 8: return launch_tsolve_t<8>(hdiag, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
+    case 16: return launch_tsolve_t<16>(hdiag, WH, Q, m, n, empty_rule, T, G, Dv, b, cnt, fb, st);
     default:
       set_error(GANQ_ERR_UNSUPPORTED, "tsolve: 2^N = %d levels unsupported (N must be 1..4)", nlev);
       return GANQ_ERR_UNSUPPORTED;
