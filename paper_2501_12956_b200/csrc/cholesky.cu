@@ -4,9 +4,9 @@
 //
 // Factorisation: right-looking blocked Cholesky with NB = 64, in place on the lower
 // triangle of A (fp64).  Per block column k: (1) one CTA factors the 64 x 64 diagonal
-// block in shared memory, (2) TRSM of the panel below it (one warp per row, forward
-// substitution, the 64 x 64 factor in shared memory), (3) trailing SYRK update of the
-// lower tiles (64 x 64 tiles, 4 x 4 fp64 register blocking, K = 64).  Each tile has one
+// block in shared memory, (2) TRSM of the panel below it (thread per row, forward
+// substitution from shared memory), (3) trailing SYRK update of the lower tiles (128 x 128 tiles,
+// 8 x 8 fp64 register blocking, K = 64).  Each tile has one
 // owner per step, so the result is deterministic (bitwise identical on every rank).
 // A non-positive pivot records its global index (atomicMin) in *d_status.
 #include <float.h>
@@ -19,6 +19,13 @@ namespace {
 
 constexpr int NB = 64;
 constexpr int LDS = NB + 1;  // padded fp64 row stride in shared memory
+
+// 8-byte global -> shared copy that does not hold a register (all of a tile's copies are in
+// flight together; cp_wait() before the barrier that publishes them)
+__device__ __forceinline__ void cp8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ---------------------------------------------------------------- precondition
 // delta_i = max(sum_j |H_ij| - 2 H_ii, 1e-8) + tau * mean(diag H)   (ADAPTIVE, Eq. 23 + R-3)
@@ -70,10 +77,14 @@ __global__ void precondition_kernel(const double* __restrict__ H, int64_t n, int
 
 // ---------------------------------------------------------------- diagonal block
 // One CTA of 256 threads = 16 x 16; thread (tx, ty) owns the 4 x 4 elements
-// (ty + 16 a, tx + 16 b) of the 64 x 64 block (no integer division in the loops).
+// (ty + 16 a, tx + 16 b) of the 64 x 64 block.  Unscaled elimination with one barrier per
+// column: step c subtracts a_rc a_qc / d_c from the trailing elements (d_c = a_cc, the pivot),
+// which equals L_rc L_qc of the standard algorithm; afterwards L_rc = a_rc / sqrt(d_c).
 __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A, int64_t n, int64_t k0,
                                                          int* __restrict__ status) {
-  __shared__ double s[NB * LDS];
+  extern __shared__ double potrf_smem[];
+  double* s = potrf_smem;               // [64][LDS] the block
+  double* dpiv = potrf_smem + NB * LDS; // [64] pivots
   const int kb = (int)min((int64_t)NB, n - k0);
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
@@ -84,35 +95,38 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A,
       s[r * LDS + c] = (r < kb && c <= r) ? A[(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
     }
   __syncthreads();
-  for (int c = 0; c < kb; ++c) {
-    double piv = s[c * LDS + c];
-    if (!(piv > 0.0)) {  // not positive definite (or NaN)
-      if (threadIdx.x == 0) atomicMin(status, (int)(k0 + c));
-      piv = 1.0;
+  for (int c = 0; c < NB; ++c) {
+    double d = s[c * LDS + c];
+    if (!(d > 0.0)) {  // not positive definite (or NaN)
+      if (threadIdx.x == 0 && c < kb) atomicMin(status, (int)(k0 + c));
+      d = 1.0;
     }
-    const double inv = 1.0 / sqrt(piv);
-    __syncthreads();  // everyone has read the pivot
-    // scale column c below the diagonal; the diagonal becomes sqrt(piv)
-    if (threadIdx.x < NB) {
-      const int r = threadIdx.x;
-      if (r > c) s[r * LDS + c] *= inv;
-      if (r == c) s[r * LDS + c] = piv * inv;
-    }
-    __syncthreads();
-    // trailing rank-1 update of the lower part (rows, cols > c)
+    if (threadIdx.x == 0) dpiv[c] = d;
+    const double id = 1.0 / d;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const int r = ty + 16 * a;
       if (r <= c) continue;
-      const double lrc = s[r * LDS + c];
+      const double arc = s[r * LDS + c] * id;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int q = tx + 16 * b;
-        if (q > c && q <= r) s[r * LDS + q] -= lrc * s[q * LDS + c];
+        if (q > c && q <= r) s[r * LDS + q] -= arc * s[q * LDS + c];
       }
     }
     __syncthreads();
   }
+  // L_rc = a_rc / sqrt(d_c), L_cc = sqrt(d_c)
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = ty + 16 * a, c = tx + 16 * b;
+      const double sd = sqrt(dpiv[c]);
+      if (c < r) s[r * LDS + c] /= sd;
+      else if (c == r) s[r * LDS + c] = sd;
+    }
+  __syncthreads();
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -123,71 +137,112 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A,
 }
 
 // ---------------------------------------------------------------- panel TRSM
-// For rows r >= k0 + kb:  L[r, k0:k0+kb] = A[r, k0:k0+kb] * L_kk^{-T}  (forward substitution).
-__global__ void __launch_bounds__(256) trsm_panel_kernel(double* __restrict__ A, int64_t n, int64_t k0) {
-  __shared__ double s[NB * LDS];
+// For rows i >= k0 + kb:  x = L[i, k0:k0+kb] solves x L_kk^T = A[i, k0:k0+kb], i.e. forward
+// substitution x_c = (a_c - sum_{q<c} x_q L_cq) / L_cc.  One thread per row (x in registers,
+// four interleaved partial sums per column), 128 rows per CTA staged through shared memory
+// (coalesced cp.async), L_kk in shared memory (broadcast reads).
+constexpr int TR = 128;
+__global__ void __launch_bounds__(TR) trsm_panel_kernel(double* __restrict__ A, int64_t n, int64_t k0) {
+  extern __shared__ double trsm_smem[];
+  double* Pr = trsm_smem;             // [TR][LDS] the CTA's panel rows
+  double* Lk = trsm_smem + TR * LDS;  // [NB][LDS] L_kk
+  double* rd = Lk + NB * LDS;         // [NB] 1 / L_cc
   const int kb = (int)min((int64_t)NB, n - k0);
-  for (int r = threadIdx.x >> 6; r < kb; r += 4) {
-    const int c = threadIdx.x & 63;
-    if (c < kb) s[r * LDS + c] = (c <= r) ? A[(k0 + r) * n + k0 + c] : 0.0;
+  const int64_t i0 = k0 + kb + (int64_t)blockIdx.x * TR;
+  for (int e = threadIdx.x; e < TR * NB; e += TR) {
+    const int r = e >> 6, c = e & 63;
+    if (i0 + r < n && c < kb) cp8(&Pr[r * LDS + c], &A[(i0 + r) * n + k0 + c]);
+    else Pr[r * LDS + c] = 0.0;
   }
+  for (int e = threadIdx.x; e < NB * NB; e += TR) {
+    const int r = e >> 6, c = e & 63;
+    if (r < kb && c <= r) cp8(&Lk[r * LDS + c], &A[(k0 + r) * n + k0 + c]);
+    else Lk[r * LDS + c] = (r == c) ? 1.0 : 0.0;
+  }
+  cp_wait();
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t row = k0 + kb + (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= n) return;
-  double* a = A + row * n + k0;
-  double x0 = (lane < kb) ? a[lane] : 0.0;
-  double x1 = (lane + 32 < kb) ? a[lane + 32] : 0.0;
-  for (int c = 0; c < kb; ++c) {
-    const double own = (c < 32) ? x0 : x1;
-    double xc = __shfl_sync(0xffffffffu, own, c & 31);
-    xc /= s[c * LDS + c];
-    if (lane == (c & 31)) { if (c < 32) x0 = xc; else x1 = xc; }
-    if (lane > c) x0 -= xc * s[lane * LDS + c];
-    if (lane + 32 > c && lane + 32 < kb) x1 -= xc * s[(lane + 32) * LDS + c];
+  if (threadIdx.x < NB) rd[threadIdx.x] = 1.0 / Lk[threadIdx.x * LDS + threadIdx.x];
+  __syncthreads();
+  const int r = threadIdx.x;
+  double x[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    double p0 = Pr[r * LDS + c], p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll
+    for (int q = 0; q + 3 < c; q += 4) {
+      p0 = fma(-x[q], Lk[c * LDS + q], p0);
+      p1 = fma(-x[q + 1], Lk[c * LDS + q + 1], p1);
+      p2 = fma(-x[q + 2], Lk[c * LDS + q + 2], p2);
+      p3 = fma(-x[q + 3], Lk[c * LDS + q + 3], p3);
+    }
+#pragma unroll
+    for (int q = c & ~3; q < c; ++q) p0 = fma(-x[q], Lk[c * LDS + q], p0);
+    x[c] = ((p0 + p1) + (p2 + p3)) * rd[c];
   }
-  if (lane < kb) a[lane] = x0;
-  if (lane + 32 < kb) a[lane + 32] = x1;
+  const int64_t i = i0 + r;
+  if (i < n) {
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+      if (c < kb) A[i * n + k0 + c] = x[c];
+  }
 }
 
 // ---------------------------------------------------------------- trailing SYRK
-// A[i, j] -= sum_c L[i, k0+c] L[j, k0+c] for the lower tiles of the trailing matrix.
+// A[i, j] -= sum_c L[i, k0+c] L[j, k0+c] for the lower 128 x 128 tiles of the trailing matrix;
+// thread (tx, ty) owns the 8 x 8 elements (ty + 16 x, tx + 16 y) of its tile.
+constexpr int ST = 128;  // SYRK tile
 __global__ void __launch_bounds__(256) syrk_trailing_kernel(double* __restrict__ A, int64_t n,
                                                             int64_t k0) {
   const int ti = blockIdx.y, tj = blockIdx.x;
   if (tj > ti) return;
   extern __shared__ double syrk_smem[];
   double* Pi = syrk_smem;
-  double* Pj = syrk_smem + NB * LDS;
+  double* Pj = syrk_smem + ST * LDS;
   const int64_t base = k0 + NB;  // first trailing row/col (only called when k0 + NB < n)
-  const int64_t i0 = base + (int64_t)ti * NB, j0 = base + (int64_t)tj * NB;
-  for (int r = threadIdx.x >> 6; r < NB; r += 4) {
-    const int c = threadIdx.x & 63;
-    Pi[r * LDS + c] = (i0 + r < n) ? A[(i0 + r) * n + k0 + c] : 0.0;
-    Pj[r * LDS + c] = (j0 + r < n) ? A[(j0 + r) * n + k0 + c] : 0.0;
+  const int64_t i0 = base + (int64_t)ti * ST, j0 = base + (int64_t)tj * ST;
+  for (int e = threadIdx.x; e < ST * NB; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    if (i0 + r < n) cp8(&Pi[r * LDS + c], &A[(i0 + r) * n + k0 + c]);
+    else Pi[r * LDS + c] = 0.0;
+    if (j0 + r < n) cp8(&Pj[r * LDS + c], &A[(j0 + r) * n + k0 + c]);
+    else Pj[r * LDS + c] = 0.0;
   }
+  cp_wait();
   __syncthreads();
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[4][4] = {};
-#pragma unroll 4
+  double acc[8][8] = {};
+#pragma unroll 2
   for (int c = 0; c < NB; ++c) {
-    double a[4], b[4];
+    double a[8], b[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) a[q] = Pi[(ty + 16 * q) * LDS + c];
+    for (int q = 0; q < 8; ++q) a[q] = Pi[(ty + 16 * q) * LDS + c];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) b[q] = Pj[(tx + 16 * q) * LDS + c];
+    for (int q = 0; q < 8; ++q) b[q] = Pj[(tx + 16 * q) * LDS + c];
+#pragma unroll
+    for (int x = 0; x < 8; ++x)
+#pragma unroll
+      for (int y = 0; y < 8; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+  }
+  // read-modify-write in two batches of 32: all loads of a batch are issued before its stores
+  // (the compiler keeps loads and stores through one pointer in order, one round trip each)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double old[4][8];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
-      for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+      for (int y = 0; y < 8; ++y) {
+        const int64_t i = i0 + ty + 16 * (4 * h + x), j = j0 + tx + 16 * y;
+        old[x][y] = (i < n && j <= i) ? A[i * n + j] : 0.0;
+      }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        const int64_t i = i0 + ty + 16 * (4 * h + x), j = j0 + tx + 16 * y;
+        if (i < n && j <= i) A[i * n + j] = old[x][y] - acc[4 * h + x][y];
+      }
   }
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      const int64_t i = i0 + ty + 16 * x, j = j0 + tx + 16 * y;
-      if (i < n && j <= i) A[i * n + j] -= acc[x][y];
-    }
 }
 
 __global__ void zero_upper_kernel(double* __restrict__ A, int64_t n) {
@@ -226,17 +281,21 @@ ganq_status_t launch_precondition(const double* H, int64_t n, int policy, double
 }
 
 ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t st) {
-  constexpr int kSyrkSmem = 2 * NB * LDS * sizeof(double);
+  constexpr int kSyrkSmem = 2 * ST * LDS * sizeof(double);
+  constexpr int kTrsmSmem = ((TR + NB) * LDS + NB) * sizeof(double);
+  constexpr int kPotrfSmem = (NB * LDS + NB) * sizeof(double);
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotrfSmem));
   GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
   for (int64_t k0 = 0; k0 < n; k0 += NB) {
-    potrf_diag_kernel<<<1, 256, 0, st>>>(A, n, k0, d_status);
+    potrf_diag_kernel<<<1, 256, kPotrfSmem, st>>>(A, n, k0, d_status);
     GANQ_LAUNCH_CHECK("potrf_diag_kernel");
     const int64_t rest = n - k0 - NB;
     if (rest <= 0) break;
-    trsm_panel_kernel<<<(unsigned)((rest + 7) / 8), 256, 0, st>>>(A, n, k0);
+    trsm_panel_kernel<<<(unsigned)((rest + TR - 1) / TR), TR, kTrsmSmem, st>>>(A, n, k0);
     GANQ_LAUNCH_CHECK("trsm_panel_kernel");
-    const unsigned T = (unsigned)((rest + NB - 1) / NB);
+    const unsigned T = (unsigned)((rest + ST - 1) / ST);
     syrk_trailing_kernel<<<dim3(T, T), 256, kSyrkSmem, st>>>(A, n, k0);
     GANQ_LAUNCH_CHECK("syrk_trailing_kernel");
   }
