@@ -57,6 +57,14 @@ def _load():
         lib.or_precondition.restype = ctypes.c_int
         lib.or_cholesky.argtypes = [P, I64, P]
         lib.or_cholesky.restype = I64
+        lib.or_pack.argtypes = [P, I64, I64, ctypes.c_int, P]
+        lib.or_pack.restype = I64
+        lib.or_unpack.argtypes = [P, I64, I64, ctypes.c_int, P]
+        lib.or_unpack.restype = None
+        lib.or_lut_gemm.argtypes = [P, P, P, I64, I64, I64, ctypes.c_int, P]
+        lib.or_lut_gemm.restype = None
+        lib.or_storage_bytes.argtypes = [I64, I64, ctypes.c_int, ctypes.c_int]
+        lib.or_storage_bytes.restype = ctypes.c_double
         lib.or_init_codebook.argtypes = [P, I64, I64, ctypes.c_int, P]
         lib.or_init_codebook.restype = None
         lib.or_sstep.argtypes = [P, P, P, I64, I64, ctypes.c_int, P, P]
@@ -202,3 +210,47 @@ def quantize(W, H, nbits, iters, policy="adaptive", lam=0.0, tau=DEFAULT_TAU, T0
     if rc >= 0:
         raise NotPositiveDefinite(rc)
     return (Q, T, tr) if trace else (Q, T)
+
+
+# --------------------------------------------------------------------------- NEXT-1
+def pack(Q, nbits: int) -> np.ndarray:
+    """Per-row little-endian N-bit packing of the codes (Table 1); rows padded
+    to whole bytes.  Raises ValueError naming the first code >= 2^N."""
+    lib = _load()
+    Q = np.ascontiguousarray(Q, dtype=np.uint8)
+    m, n = Q.shape
+    out = np.zeros((m, (n * nbits + 7) // 8), dtype=np.uint8)
+    bad = lib.or_pack(Q.ctypes.data, m, n, nbits, out.ctypes.data)
+    if bad >= 0:
+        raise ValueError(f"code {int(Q.flat[bad])} at flat index {bad} >= 2^{nbits}")
+    return out
+
+
+def unpack(Pk, m: int, n: int, nbits: int) -> np.ndarray:
+    lib = _load()
+    Pk = np.ascontiguousarray(Pk, dtype=np.uint8)
+    Q = np.zeros((m, n), dtype=np.uint8)
+    lib.or_unpack(Pk.ctypes.data, m, n, nbits, Q.ctypes.data)
+    return Q
+
+
+def lut_gemm(Pk, T16, X16, m: int, n: int, nbits: int) -> np.ndarray:
+    """Y (p x m, fp64) = X W~^T, W~_ij = T16[i][Q_ij] (Fig. 1a right).
+    T16 (m x 2^N) and X16 (p x n) are float16 arrays."""
+    lib = _load()
+    Pk = np.ascontiguousarray(Pk, dtype=np.uint8)
+    T16 = np.ascontiguousarray(T16, dtype=np.float16)
+    X16 = np.ascontiguousarray(X16, dtype=np.float16)
+    p = X16.shape[0]
+    Y = np.zeros((p, m), dtype=np.float64)
+    lib.or_lut_gemm(Pk.ctypes.data, T16.view(np.uint16).ctypes.data, X16.view(np.uint16).ctypes.data,
+                    m, n, p, nbits, Y.ctypes.data)
+    return Y
+
+
+STORAGE = {"fp16": 0, "uniform": 1, "lut": 2}
+
+
+def storage_bytes(m: int, n: int, nbits: int, scheme: str) -> float:
+    """Table 1: fp16 2mn; uniform mnN/8 + 4m; LUT mnN/8 + 2*2^N*m."""
+    return _load().or_storage_bytes(m, n, nbits, STORAGE[scheme])

@@ -435,3 +435,82 @@ int64_t or_quantize(const double *W, int64_t m, int64_t n, const double *H, int 
     free(Tk); free(Tn); free(L);
     return -1;
 }
+
+/* ========================================================================= */
+/* NEXT-1: the inference side of Fig. 1a.                */
+/* ========================================================================= */
+
+/* Packing of Q ("a low-bit query matrix Q in {0..2^N-1}^{m x n}"), in the layout of
+ * the storage accounting of Table 1: row i is a little-endian bitstream in which
+ * code k occupies bits [k N, (k+1) N); each row is padded to a whole byte, so a row takes
+ * ceil(n N / 8) bytes.  Returns -1, or the flat index of the first code >= 2^N (argument
+ * error; nothing is written past it). */
+int64_t or_pack(const uint8_t *Q, int64_t m, int64_t n, int N, uint8_t *P) {
+    const int64_t rb = (n * N + 7) / 8;
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t k = 0; k < n; ++k)
+            if (Q[i * n + k] >= (1u << N)) return i * n + k;
+    memset(P, 0, (size_t)(m * rb));
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t k = 0; k < n; ++k)
+            for (int b = 0; b < N; ++b) {
+                const int64_t bit = k * N + b;
+                if ((Q[i * n + k] >> b) & 1u) P[i * rb + bit / 8] |= (uint8_t)(1u << (bit % 8));
+            }
+    return -1;
+}
+
+void or_unpack(const uint8_t *P, int64_t m, int64_t n, int N, uint8_t *Q) {
+    const int64_t rb = (n * N + 7) / 8;
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t k = 0; k < n; ++k) {
+            unsigned v = 0;
+            for (int b = 0; b < N; ++b) {
+                const int64_t bit = k * N + b;
+                v |= (unsigned)((P[i * rb + bit / 8] >> (bit % 8)) & 1u) << b;
+            }
+            Q[i * n + k] = (uint8_t)v;
+        }
+}
+
+/* IEEE binary16 -> double, exact (Table 1 stores the codebook in fp16). */
+static double half_to_double(uint16_t h) {
+    const int s = (h >> 15) & 1, e = (h >> 10) & 31, f = h & 1023;
+    double v;
+    if (e == 0) v = ldexp((double)f, -24);                   /* subnormal */
+    else if (e == 31) v = f ? NAN : INFINITY;
+    else v = ldexp((double)(f | 1024), e - 25);
+    return s ? -v : v;
+}
+
+/* LUT-based mpGEMM (Fig. 1a right; W~_ij = t_{i, Q_ij}):
+ *   Y[t][i] = sum_j W~_ij X[t][j] = sum_j T16[i][Q_ij] X[t][j]
+ * T16: m x 2^N fp16 codebook, X: p x n fp16 activations (token-major), Y: p x m, fp64,
+ * the codes read from the packed rows one by one (no dense W~ is formed). */
+void or_lut_gemm(const uint8_t *P, const uint16_t *T16, const uint16_t *X, int64_t m, int64_t n,
+                 int64_t p, int N, double *Y) {
+    const int64_t rb = (n * N + 7) / 8, nl = (int64_t)1 << N;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t t = 0; t < p; ++t) {
+            double acc = 0.0;
+            for (int64_t j = 0; j < n; ++j) {
+                unsigned q = 0;
+                for (int b = 0; b < N; ++b) {
+                    const int64_t bit = j * N + b;
+                    q |= (unsigned)((P[i * rb + bit / 8] >> (bit % 8)) & 1u) << b;
+                }
+                acc += half_to_double(T16[i * nl + q]) * half_to_double(X[t * n + j]);
+            }
+            Y[t * m + i] = acc;
+        }
+}
+
+/* Storage of an m x n weight matrix, Table 1: fp16 2mn; per-channel uniform N-bit
+ * mn N / 8 + 4m (fp16 scale and zero point); LUT mn N / 8 + 2 * 2^N m (fp16 codebook). */
+double or_storage_bytes(int64_t m, int64_t n, int N, int scheme) {
+    const double q = (double)m * (double)n * N / 8.0;
+    if (scheme == 0) return 2.0 * (double)m * (double)n;
+    if (scheme == 1) return q + 4.0 * (double)m;
+    return q + 2.0 * (double)(1 << N) * (double)m;
+}
