@@ -163,6 +163,35 @@ const char* ganq_last_error(void);
 /* Failing pivot index for GANQ_ERR_NOT_PD, else -1. */
 int64_t ganq_last_error_index(void);
 /* Library version string. */
+/*
+ * ---------------------------------------------------------------- NEXT-1: deployment side
+ * LUT-based mixed-precision GEMM, Fig. 1a right: W~_ij = t_{i, Q_ij} is never
+ * formed; the kernel gathers codebook entries by the packed codes.  Storage as in Table 1
+ * (P:87-99): codes N bits each, codebook fp16 (2 * 2^N bytes per row).
+ *
+ * Packed layout: row i is a little-endian bitstream, code k in bits [k N, (k+1) N), padded to
+ * whole bytes: ganq_packed_row_bytes(n, N) = ceil(n N / 8) bytes per row, rows contiguous.
+ * fp16 values are passed as their IEEE binary16 bit patterns (uint16_t).
+ */
+int64_t ganq_packed_row_bytes(int64_t n, int n_bits);
+
+/* Q (m x n codes, < 2^n_bits; larger values are undefined -- only their low n_bits bits are
+ * stored) -> packed (m x ganq_packed_row_bytes(n, n_bits)).  Async on `stream`.
+ * INVALID_ARG: m, n < 1, n_bits not in [1, 8], null pointers. */
+ganq_status_t ganq_pack_codes(const uint8_t* Q, int64_t m, int64_t n, int n_bits, uint8_t* packed,
+                              void* stream);
+
+/* T (m x 2^n_bits fp32) -> T16 (m x 2^n_bits fp16, round to nearest even).  Async. */
+ganq_status_t ganq_codebook_f16(const float* T, int64_t m, int n_bits, uint16_t* T16, void* stream);
+
+/* Y (p x m, fp32) = X W~^T with X (p x n, fp16, token-major), W~_ij = T16[i][Q_ij] decoded
+ * from `packed`.  Each output is accumulated in fp32 in a fixed order (a lane's codes in
+ * ascending j, then a fixed butterfly over the 32 lanes of a warp), so results are
+ * reproducible run to run.  Intended for decode (p small); p is processed in blocks of 8.
+ * Async.  INVALID_ARG: m, n, p < 1, n_bits not in [1, 8], null pointers. */
+ganq_status_t ganq_lut_gemm(const uint8_t* packed, const uint16_t* T16, const uint16_t* X, int64_t m,
+                            int64_t n, int64_t p, int n_bits, float* Y, void* stream);
+
 const char* ganq_version(void);
 
 #ifdef __cplusplus

@@ -7,10 +7,12 @@ Public API (torch CUDA tensors; thin binding of include/ganq.h):
     tstep(W, Q, H, n_bits)             closed-form T-update  Eq. (6)
     factor(H)                          L = chol(H')          Eq. (9) + App. A
     dist.quantize_layer_distributed    token-sharded H + row-sharded solve over NCCL
+    pack_codes / codebook_f16 / lut_gemm   NEXT-1: N-bit storage and LUT mpGEMM (Fig. 1a)
 """
-from .api import (factor, hessian, objective, objective_workspace_size, quantize_layer, tstep,
-                  version, workspace_size)
+from .api import (codebook_f16, factor, hessian, lut_gemm, objective, objective_workspace_size,
+                  pack_codes, quantize_layer, tstep, version, workspace_size)
 from ._lib import GanqError, NotPositiveDefinite
 
 __all__ = ["hessian", "quantize_layer", "objective", "tstep", "factor", "workspace_size",
-           "objective_workspace_size", "version", "GanqError", "NotPositiveDefinite"]
+           "objective_workspace_size", "version", "pack_codes", "codebook_f16", "lut_gemm", "GanqError",
+           "NotPositiveDefinite"]

@@ -39,6 +39,10 @@ SIG = {
     "ganq_last_error": (ctypes.c_char_p, []),
     "ganq_last_error_index": (I64, []),
     "ganq_version": (ctypes.c_char_p, []),
+    "ganq_packed_row_bytes": (I64, [I64, I32]),
+    "ganq_pack_codes": (I32, [P, I64, I64, I32, P, P]),
+    "ganq_codebook_f16": (I32, [P, I64, I32, P, P]),
+    "ganq_lut_gemm": (I32, [P, P, P, I64, I64, I64, I32, P, P]),
 }
 
 

@@ -14,7 +14,7 @@ import torch
 from . import _lib
 
 __all__ = ["hessian", "quantize_layer", "objective", "tstep", "factor", "workspace_size",
-           "objective_workspace_size", "version"]
+           "objective_workspace_size", "version", "pack_codes", "codebook_f16", "lut_gemm"]
 
 
 def _ptr(t):
@@ -165,3 +165,46 @@ def factor(H, precond: str = "adaptive", lam: float = 0.0, tau: float = 1e-7, st
     _lib.check(lib.ganq_factor(_ptr(H), n, ctypes.byref(o), _ptr(L), _ptr(delta), _ptr(ws), ws.numel(),
                                _stream(stream)))
     return L, delta
+
+
+# --------------------------------------------------------------------------- NEXT-1
+def pack_codes(Q, n_bits: int, stream=None, check: bool = True):
+    """Per-row little-endian N-bit packing of Q (Table 1 storage) -> uint8 m x ceil(nN/8).
+
+    check=True verifies on the device that every code is < 2^N (the kernel stores only the low
+    N bits of a code) and raises ValueError otherwise."""
+    _need(Q, torch.uint8, 2, "Q")
+    m, n = Q.shape
+    if check and int(Q.max()) >= (1 << n_bits):
+        raise ValueError(f"codes must be < 2^{n_bits}")
+    lib = _lib.load()
+    P = torch.empty((m, int(lib.ganq_packed_row_bytes(n, int(n_bits)))), dtype=torch.uint8, device=Q.device)
+    _lib.check(lib.ganq_pack_codes(_ptr(Q), m, n, int(n_bits), _ptr(P), _stream(stream)))
+    return P
+
+
+def codebook_f16(T, stream=None):
+    """fp32 codebook (m x 2^N) -> fp16 (round to nearest even), the stored form of Table 1."""
+    _need(T, torch.float32, 2, "T")
+    m, nl = T.shape
+    n_bits = int(nl).bit_length() - 1
+    T16 = torch.empty((m, nl), dtype=torch.float16, device=T.device)
+    _lib.check(_lib.load().ganq_codebook_f16(_ptr(T), m, n_bits, _ptr(T16), _stream(stream)))
+    return T16
+
+
+def lut_gemm(P, T16, X, n: int, Y=None, stream=None):
+    """Y (p x m, fp32) = X W~^T for W~_ij = T16[i][Q_ij] decoded from the packed codes
+    (Fig. 1a right).  X: p x n fp16 (token-major)."""
+    _need(P, torch.uint8, 2, "packed")
+    _need(T16, torch.float16, 2, "T16")
+    _need(X, torch.float16, 2, "X")
+    m, nl = T16.shape
+    n_bits = int(nl).bit_length() - 1
+    p = X.shape[0]
+    if X.shape[1] != n:
+        raise ValueError("X must be p x n")
+    if Y is None:
+        Y = torch.empty((p, m), dtype=torch.float32, device=X.device)
+    _lib.check(_lib.load().ganq_lut_gemm(_ptr(P), _ptr(T16), _ptr(X), m, n, p, n_bits, _ptr(Y), _stream(stream)))
+    return Y

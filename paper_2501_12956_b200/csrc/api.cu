@@ -266,6 +266,43 @@ int64_t ganq_launch_count(void) { return g_launches.load(); }
 
 const char* ganq_last_error(void) { return g_msg; }
 int64_t ganq_last_error_index(void) { return g_index; }
+int64_t ganq_packed_row_bytes(int64_t n, int n_bits) {
+  if (n < 1 || n_bits < 1 || n_bits > 8) return 0;
+  return (n * n_bits + 7) / 8;
+}
+
+ganq_status_t ganq_pack_codes(const uint8_t* Q, int64_t m, int64_t n, int n_bits, uint8_t* packed,
+                              void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (m < 1 || n < 1 || n_bits < 1 || n_bits > 8 || !Q || !packed) {
+    set_error(GANQ_ERR_INVALID_ARG, "pack_codes: need m, n >= 1, n_bits in [1, 8], non-null buffers");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  return launch_pack_codes(Q, m, n, n_bits, packed, (cudaStream_t)stream);
+}
+
+ganq_status_t ganq_codebook_f16(const float* T, int64_t m, int n_bits, uint16_t* T16, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (m < 1 || n_bits < 1 || n_bits > 8 || !T || !T16) {
+    set_error(GANQ_ERR_INVALID_ARG, "codebook_f16: need m >= 1, n_bits in [1, 8], non-null buffers");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  return launch_codebook_f16(T, m * ((int64_t)1 << n_bits), T16, (cudaStream_t)stream);
+}
+
+ganq_status_t ganq_lut_gemm(const uint8_t* packed, const uint16_t* T16, const uint16_t* X, int64_t m,
+                            int64_t n, int64_t p, int n_bits, float* Y, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (m < 1 || n < 1 || p < 1 || n_bits < 1 || n_bits > 8 || !packed || !T16 || !X || !Y) {
+    set_error(GANQ_ERR_INVALID_ARG, "lut_gemm: need m, n, p >= 1, n_bits in [1, 8], non-null buffers");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  return launch_lut_gemm(packed, T16, X, m, n, p, n_bits, Y, (cudaStream_t)stream);
+}
+
 const char* ganq_version(void) { return "ganq-b200 0.1 (sm_100a)"; }
 
 ganq_status_t ganq_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate,

@@ -48,6 +48,11 @@ ganq_status_t launch_hdiag(const double* H, int64_t n, double* hdiag, cudaStream
 ganq_status_t launch_tsolve(const double* hdiag, const float* WH, const uint8_t* Q, int64_t m, int64_t n, int nlev,
                             int empty_rule, float* T, double* G, double* Dv, double* b, int* cnt, int* fallback,
                             cudaStream_t st);
+// lut.cu (NEXT-1)
+ganq_status_t launch_pack_codes(const uint8_t* Q, int64_t m, int64_t n, int N, uint8_t* P, cudaStream_t st);
+ganq_status_t launch_codebook_f16(const float* T, int64_t total, uint16_t* T16, cudaStream_t st);
+ganq_status_t launch_lut_gemm(const uint8_t* P, const uint16_t* T16, const uint16_t* X, int64_t m, int64_t n,
+                              int64_t p, int N, float* Y, cudaStream_t st);
 // tgram_tc.cu
 int64_t tq_pitch(int64_t n);
 ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* scale, cudaStream_t st);

@@ -1,0 +1,188 @@
+// lut.cu -- NEXT-1, the deployment side of GANQ: N-bit packing of the codes and the LUT-based
+// mixed-precision GEMM of Fig. 1a right, W~_ij = t_{i, Q_ij}, storage as in
+// Table 1 (fp16 codebook, N bits per code).
+//
+// lut_gemm: one warp per row of W~ (grid-stride).  A row's packed codes are read once from
+// HBM (coalesced: lane l takes the 8 codes [256 c + 8 l, +8) of chunk c, N bytes); the row's
+// 2^N codebook entries sit as fp32 in 16 distinct shared-memory banks (a lookup is one
+// conflict-free LDS); X (p x n fp16, L2-resident) is staged once per CTA in shared memory.
+// Each lane accumulates its codes in ascending j in fp32, then a fixed butterfly over the
+// warp: deterministic.  HBM-bound: n N / 8 + 2^{N+1} bytes per row.
+#include <cuda_fp16.h>
+
+#include "ganq_internal.cuh"
+
+namespace ganq {
+namespace {
+
+constexpr int LUT_WARPS = 8;
+constexpr int LUT_PMAX = 8;  // tokens per launch (decode)
+
+__global__ void pack_kernel(const uint8_t* __restrict__ Q, int64_t m, int64_t n, int N,
+                            uint8_t* __restrict__ P) {
+  const int64_t rb = (n * N + 7) / 8, groups = (n + 7) / 8;
+  const uint32_t mask = (1u << N) - 1u;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < m * groups;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / groups, g = idx % groups;
+    const int64_t k0 = 8 * g;
+    const int cnt = (int)min((int64_t)8, n - k0);
+    uint64_t v = 0;
+    for (int k = 0; k < cnt; ++k) v |= (uint64_t)(Q[i * n + k0 + k] & mask) << (k * N);
+    const int nbytes = (cnt * N + 7) / 8;  // 8 codes = N whole bytes
+    uint8_t* dst = P + i * rb + g * N;
+    for (int b = 0; b < nbytes; ++b) dst[b] = (uint8_t)(v >> (8 * b));
+  }
+}
+
+__global__ void codebook_f16_kernel(const float* __restrict__ T, int64_t total, __half* __restrict__ T16) {
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    T16[idx] = __float2half_rn(T[idx]);
+}
+
+template <int N, int PT>
+__global__ void __launch_bounds__(32 * LUT_WARPS)
+lut_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, const __half* __restrict__ X,
+                int64_t m, int64_t n, int64_t p, float* __restrict__ Y) {
+  extern __shared__ __align__(16) uint8_t lut_smem[];
+  constexpr int NL = 1 << N;
+  float* sT = reinterpret_cast<float*>(lut_smem);              // [LUT_WARPS][NL]
+  __half* sX = reinterpret_cast<__half*>(sT + LUT_WARPS * NL);  // [PT][npad]
+  const int64_t npad = (n + 255) / 256 * 256;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t e = threadIdx.x; e < PT * npad; e += blockDim.x) {
+    const int64_t t = e / npad, j = e % npad;
+    sX[e] = (t < p && j < n) ? X[t * n + j] : __float2half_rn(0.0f);
+  }
+  __syncthreads();
+  const int64_t rb = (n * N + 7) / 8;
+  const int64_t chunks = npad / 256;
+  const uint32_t mask = NL - 1;
+  for (int64_t row = (int64_t)blockIdx.x * LUT_WARPS + warp; row < m; row += (int64_t)gridDim.x * LUT_WARPS) {
+    for (int e = lane; e < NL; e += 32) sT[warp * NL + e] = __half2float(T16[row * NL + e]);
+    __syncwarp();
+    const uint8_t* prow = P + row * rb;
+    float acc[PT];
+#pragma unroll
+    for (int t = 0; t < PT; ++t) acc[t] = 0.0f;
+    for (int64_t c = 0; c < chunks; ++c) {
+      const int64_t j0 = 256 * c + 8 * lane;  // this lane's first code in the chunk
+      const int64_t b0 = j0 * N / 8;          // its first byte (8 codes = N whole bytes)
+      uint64_t bits = 0;
+      if (j0 + 8 <= n) {
+        if constexpr (N == 4) {
+          bits = (reinterpret_cast<uintptr_t>(prow + b0) & 3) == 0
+                     ? *reinterpret_cast<const uint32_t*>(prow + b0)
+                     : (uint64_t)prow[b0] | ((uint64_t)prow[b0 + 1] << 8) | ((uint64_t)prow[b0 + 2] << 16) |
+                           ((uint64_t)prow[b0 + 3] << 24);
+        } else {
+#pragma unroll
+          for (int b = 0; b < N; ++b) bits |= (uint64_t)prow[b0 + b] << (8 * b);
+        }
+      } else if (j0 < n) {
+        const int64_t nb = ((n - j0) * N + 7) / 8;
+        for (int b = 0; b < nb; ++b) bits |= (uint64_t)prow[b0 + b] << (8 * b);
+      }
+      float w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = (j0 + k < n) ? sT[warp * NL + ((bits >> (k * N)) & mask)] : 0.0f;
+#pragma unroll
+      for (int t = 0; t < PT; ++t) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(sX + t * npad + j0);  // 8 halfs
+        const __half2* xh = reinterpret_cast<const __half2*>(&xv);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) {
+          const float2 xf = __half22float2(xh[k2]);
+          acc[t] = fmaf(w[2 * k2], xf.x, acc[t]);
+          acc[t] = fmaf(w[2 * k2 + 1], xf.y, acc[t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < PT; ++t)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < PT; ++t)
+        if (t < p) Y[t * m + row] = acc[t];
+    }
+    __syncwarp();
+  }
+}
+
+template <int N, int PT>
+ganq_status_t launch_lut_t(const uint8_t* P, const __half* T16, const __half* X, int64_t m, int64_t n, int64_t p,
+                           float* Y, cudaStream_t st) {
+  const int64_t npad = (n + 255) / 256 * 256;
+  const size_t smem = (size_t)LUT_WARPS * (1 << N) * sizeof(float) + (size_t)PT * npad * sizeof(__half);
+  if (smem > 227 * 1024) {
+    set_error(GANQ_ERR_UNSUPPORTED, "lut_gemm: n = %lld too large for the shared-memory staging of X",
+              (long long)n);
+    return GANQ_ERR_UNSUPPORTED;
+  }
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(lut_gemm_kernel<N, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lut_gemm_kernel<N, PT>, 32 * LUT_WARPS, smem);
+  const int64_t want = (m + LUT_WARPS - 1) / LUT_WARPS;
+  const unsigned grid = (unsigned)min(want, (int64_t)sms * (per_sm > 0 ? per_sm : 1));
+  lut_gemm_kernel<N, PT><<<grid, 32 * LUT_WARPS, smem, st>>>(P, T16, X, m, n, p, Y);
+  GANQ_LAUNCH_CHECK("lut_gemm_kernel");
+  return GANQ_OK;
+}
+
+template <int N>
+ganq_status_t launch_lut_n(const uint8_t* P, const __half* T16, const __half* X, int64_t m, int64_t n, int64_t p,
+                           float* Y, cudaStream_t st) {
+  for (int64_t t0 = 0; t0 < p; t0 += LUT_PMAX) {
+    const int64_t pb = min((int64_t)LUT_PMAX, p - t0);
+    ganq_status_t s;
+    const __half* Xb = X + t0 * n;
+    float* Yb = Y + t0 * m;
+    if (pb == 1) s = launch_lut_t<N, 1>(P, T16, Xb, m, n, pb, Yb, st);
+    else if (pb == 2) s = launch_lut_t<N, 2>(P, T16, Xb, m, n, pb, Yb, st);
+    else if (pb <= 4) s = launch_lut_t<N, 4>(P, T16, Xb, m, n, pb, Yb, st);
+    else s = launch_lut_t<N, 8>(P, T16, Xb, m, n, pb, Yb, st);
+    if (s) return s;
+  }
+  return GANQ_OK;
+}
+
+}  // namespace
+
+ganq_status_t launch_pack_codes(const uint8_t* Q, int64_t m, int64_t n, int N, uint8_t* P, cudaStream_t st) {
+  pack_kernel<<<1184, 256, 0, st>>>(Q, m, n, N, P);
+  GANQ_LAUNCH_CHECK("pack_kernel");
+  return GANQ_OK;
+}
+
+ganq_status_t launch_codebook_f16(const float* T, int64_t total, uint16_t* T16, cudaStream_t st) {
+  codebook_f16_kernel<<<(unsigned)min((int64_t)1184, (total + 255) / 256), 256, 0, st>>>(
+      T, total, reinterpret_cast<__half*>(T16));
+  GANQ_LAUNCH_CHECK("codebook_f16_kernel");
+  return GANQ_OK;
+}
+
+ganq_status_t launch_lut_gemm(const uint8_t* P, const uint16_t* T16, const uint16_t* X, int64_t m, int64_t n,
+                              int64_t p, int N, float* Y, cudaStream_t st) {
+  const __half* t = reinterpret_cast<const __half*>(T16);
+  const __half* x = reinterpret_cast<const __half*>(X);
+  switch (N) {
+    case 1: return launch_lut_n<1>(P, t, x, m, n, p, Y, st);
+    case 2: return launch_lut_n<2>(P, t, x, m, n, p, Y, st);
+    case 3: return launch_lut_n<3>(P, t, x, m, n, p, Y, st);
+    case 4: return launch_lut_n<4>(P, t, x, m, n, p, Y, st);
+    case 5: return launch_lut_n<5>(P, t, x, m, n, p, Y, st);
+    case 6: return launch_lut_n<6>(P, t, x, m, n, p, Y, st);
+    case 7: return launch_lut_n<7>(P, t, x, m, n, p, Y, st);
+    case 8: return launch_lut_n<8>(P, t, x, m, n, p, Y, st);
+    default:
+      set_error(GANQ_ERR_INVALID_ARG, "lut_gemm: n_bits = %d not in [1, 8]", N);
+      return GANQ_ERR_INVALID_ARG;
+  }
+}
+
+}  // namespace ganq

@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "ganq.h")
 def declared_symbols():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(ganq_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ganq_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
@@ -93,3 +93,16 @@ def test_binding_rejects_cpu_tensors():
         g.hessian(torch.zeros((4, 8), dtype=torch.bfloat16))
     with pytest.raises(ValueError, match="CUDA"):
         g.quantize_layer(torch.zeros((4, 8)), torch.zeros((8, 8), dtype=torch.float64), 2, 1)
+
+
+def test_lut_binding_rejects_host_tensors():
+    import torch
+    import paper_2501_12956_b200 as g
+    with pytest.raises(ValueError, match="CUDA"):
+        g.pack_codes(torch.zeros((2, 8), dtype=torch.uint8), 4)
+
+
+def test_packed_row_bytes(lib):
+    assert lib.ganq_packed_row_bytes(4096, 4) == 2048
+    assert lib.ganq_packed_row_bytes(7, 3) == 3
+    assert lib.ganq_packed_row_bytes(0, 4) == 0 and lib.ganq_packed_row_bytes(5, 9) == 0
