@@ -9,6 +9,7 @@
 // Each lane accumulates its codes in ascending j in fp32, then a fixed butterfly over the
 // warp: deterministic.  HBM-bound: n N / 8 + 2^{N+1} bytes per row.
 #include <cuda_fp16.h>
+#include <stdlib.h>
 
 #include "ganq_internal.cuh"
 
@@ -17,6 +18,7 @@ namespace {
 
 constexpr int LUT_WARPS = 8;
 constexpr int LUT_PMAX = 8;  // tokens per launch (decode)
+constexpr int LUT_CH = 16;   // chunks of 256 codes whose loads are issued together
 
 __global__ void pack_kernel(const uint8_t* __restrict__ Q, int64_t m, int64_t n, int N,
                             uint8_t* __restrict__ P) {
@@ -51,11 +53,25 @@ lut_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, c
   __half* sX = reinterpret_cast<__half*>(sT + LUT_WARPS * NL);  // [PT][npad]
   const int64_t npad = (n + 255) / 256 * 256;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t e = threadIdx.x; e < PT * npad; e += blockDim.x) {
-    const int64_t t = e / npad, j = e % npad;
-    sX[e] = (t < p && j < n) ? X[t * n + j] : __float2half_rn(0.0f);
+  // p = 1 reads its activations straight from global memory (8 KB, L1/L2-resident), issued
+  // with the codes; p > 1 stages X in shared memory once per CTA (16-byte loads when aligned)
+  const bool xvec = (n & 7) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  if constexpr (PT > 1) {
+    if (xvec) {
+      for (int64_t e = threadIdx.x; e < PT * npad / 8; e += blockDim.x) {
+        const int64_t t = (8 * e) / npad, j = (8 * e) % npad;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (t < p && j < n) v = __ldg(reinterpret_cast<const uint4*>(X + t * n + j));
+        *reinterpret_cast<uint4*>(sX + 8 * e) = v;
+      }
+    } else {
+      for (int64_t e = threadIdx.x; e < PT * npad; e += blockDim.x) {
+        const int64_t t = e / npad, j = e % npad;
+        sX[e] = (t < p && j < n) ? X[t * n + j] : __float2half_rn(0.0f);
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int64_t rb = (n * N + 7) / 8;
   const int64_t chunks = npad / 256;
   const uint32_t mask = NL - 1;
@@ -66,36 +82,63 @@ lut_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, c
     float acc[PT];
 #pragma unroll
     for (int t = 0; t < PT; ++t) acc[t] = 0.0f;
-    for (int64_t c = 0; c < chunks; ++c) {
+    // the codes of LUT_CH chunks are loaded first (independent loads in flight), then used
+    auto load_bits = [&](int64_t c) -> uint64_t {
       const int64_t j0 = 256 * c + 8 * lane;  // this lane's first code in the chunk
       const int64_t b0 = j0 * N / 8;          // its first byte (8 codes = N whole bytes)
       uint64_t bits = 0;
       if (j0 + 8 <= n) {
         if constexpr (N == 4) {
           bits = (reinterpret_cast<uintptr_t>(prow + b0) & 3) == 0
-                     ? *reinterpret_cast<const uint32_t*>(prow + b0)
+                     ? __ldg(reinterpret_cast<const uint32_t*>(prow + b0))
                      : (uint64_t)prow[b0] | ((uint64_t)prow[b0 + 1] << 8) | ((uint64_t)prow[b0 + 2] << 16) |
                            ((uint64_t)prow[b0 + 3] << 24);
         } else {
 #pragma unroll
-          for (int b = 0; b < N; ++b) bits |= (uint64_t)prow[b0 + b] << (8 * b);
+          for (int b = 0; b < N; ++b) bits |= (uint64_t)__ldg(prow + b0 + b) << (8 * b);
         }
       } else if (j0 < n) {
         const int64_t nb = ((n - j0) * N + 7) / 8;
         for (int b = 0; b < nb; ++b) bits |= (uint64_t)prow[b0 + b] << (8 * b);
       }
-      float w[8];
+      return bits;
+    };
+    for (int64_t c0 = 0; c0 < chunks; c0 += LUT_CH) {
+      uint64_t bits[LUT_CH];
+      uint4 xg[PT == 1 ? LUT_CH : 1];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) w[k] = (j0 + k < n) ? sT[warp * NL + ((bits >> (k * N)) & mask)] : 0.0f;
+      for (int u = 0; u < LUT_CH; ++u) {
+        bits[u] = (c0 + u < chunks) ? load_bits(c0 + u) : 0;
+        if constexpr (PT == 1) {
+          const int64_t j0 = 256 * (c0 + u) + 8 * lane;
+          if (xvec && j0 + 8 <= n) {
+            xg[u] = __ldg(reinterpret_cast<const uint4*>(X + j0));
+          } else {
+            __half h[8];
 #pragma unroll
-      for (int t = 0; t < PT; ++t) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(sX + t * npad + j0);  // 8 halfs
-        const __half2* xh = reinterpret_cast<const __half2*>(&xv);
+            for (int k = 0; k < 8; ++k) h[k] = (j0 + k < n) ? X[j0 + k] : __float2half_rn(0.0f);
+            xg[u] = *reinterpret_cast<const uint4*>(h);
+          }
+        }
+      }
 #pragma unroll
-        for (int k2 = 0; k2 < 4; ++k2) {
-          const float2 xf = __half22float2(xh[k2]);
-          acc[t] = fmaf(w[2 * k2], xf.x, acc[t]);
-          acc[t] = fmaf(w[2 * k2 + 1], xf.y, acc[t]);
+      for (int u = 0; u < LUT_CH; ++u) {
+        if (c0 + u >= chunks) break;
+        const int64_t j0 = 256 * (c0 + u) + 8 * lane;
+        float w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          w[k] = (j0 + k < n) ? sT[warp * NL + ((bits[u] >> (k * N)) & mask)] : 0.0f;
+#pragma unroll
+        for (int t = 0; t < PT; ++t) {
+          const uint4 xv = (PT == 1) ? xg[u] : *reinterpret_cast<const uint4*>(sX + t * npad + j0);  // 8 halfs
+          const __half2* xh = reinterpret_cast<const __half2*>(&xv);
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            const float2 xf = __half22float2(xh[k2]);
+            acc[t] = fmaf(w[2 * k2], xf.x, acc[t]);
+            acc[t] = fmaf(w[2 * k2 + 1], xf.y, acc[t]);
+          }
         }
       }
     }
@@ -112,11 +155,126 @@ lut_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, c
   }
 }
 
+// Fast path for the common shape: N = 4, n a multiple of 256 (whole chunks, 4-byte aligned code
+// words), X 16-byte aligned.  Same arithmetic and summation order as lut_gemm_kernel (a lane's
+// codes in ascending j, fmaf into fp32, then the butterfly), without per-code bounds checks.
+template <int PT>
+__global__ void __launch_bounds__(32 * LUT_WARPS)
+lut4_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, const __half* __restrict__ X,
+                 int m, int n, int p, float* __restrict__ Y) {
+  __shared__ __align__(512) float sT[LUT_WARPS * 16];
+  extern __shared__ __align__(16) float sXf[];  // [PT][n] fp32 (converted once per CTA)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunks0 = n >> 8, rb0 = n >> 1;
+  // the first row's codes and codebook entry are requested before X is staged (overlap)
+  uint32_t bn[LUT_CH];
+  float tn = 0.0f;
+  auto prefetch = [&](int r) {
+    const uint32_t* pr = reinterpret_cast<const uint32_t*>(P + (int64_t)r * rb0);
+#pragma unroll
+    for (int u = 0; u < LUT_CH; ++u) bn[u] = (u < chunks0) ? __ldg(pr + 32 * u + lane) : 0u;  // 128 B per chunk
+    tn = __half2float(T16[(int64_t)r * 16 + (lane & 15)]);
+  };
+  if (blockIdx.x * LUT_WARPS + warp < m) prefetch(blockIdx.x * LUT_WARPS + warp);
+  for (int e = threadIdx.x; e < PT * n / 8; e += blockDim.x) {
+    const int t = (8 * e) / n, j = (8 * e) % n;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t < p) v = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)t * n + j));
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+    float4 f0, f1;
+    f0.x = __low2float(h[0]); f0.y = __high2float(h[0]); f0.z = __low2float(h[1]); f0.w = __high2float(h[1]);
+    f1.x = __low2float(h[2]); f1.y = __high2float(h[2]); f1.z = __low2float(h[3]); f1.w = __high2float(h[3]);
+    reinterpret_cast<float4*>(sXf + 8 * e)[0] = f0;
+    reinterpret_cast<float4*>(sXf + 8 * e)[1] = f1;
+  }
+  __syncthreads();
+  const int chunks = n >> 8, rb = n >> 1;
+  // shared address of this warp's 16 fp32 entries (64-byte aligned), OR-ed with (code * 4): the
+  // address of a lookup is one LOP3 of the shifted code word
+  const uint32_t tsh = smem_u32(sT) + (uint32_t)warp * 64u;
+  // rows are software-pipelined per warp: the codes of the first LUT_CH chunks and the codebook
+  // entry of the next row are in flight while the current row is computed
+  const int stride = gridDim.x * LUT_WARPS;
+  int row = blockIdx.x * LUT_WARPS + warp;
+  for (; row < m; row += stride) {
+    uint32_t b0[LUT_CH];
+#pragma unroll
+    for (int u = 0; u < LUT_CH; ++u) b0[u] = bn[u];
+    if (lane < 16) sT[warp * 16 + lane] = tn;
+    if (row + stride < m) prefetch(row + stride);
+    __syncwarp();
+    const uint32_t* prow = reinterpret_cast<const uint32_t*>(P + (int64_t)row * rb);
+    float acc[PT];
+#pragma unroll
+    for (int t = 0; t < PT; ++t) acc[t] = 0.0f;
+    for (int c0 = 0; c0 < chunks; c0 += LUT_CH) {
+      uint32_t b[LUT_CH];
+#pragma unroll
+      for (int u = 0; u < LUT_CH; ++u)
+        b[u] = (c0 == 0) ? b0[u] : ((c0 + u < chunks) ? __ldg(prow + 32 * (c0 + u) + lane) : 0u);
+#pragma unroll
+      for (int u = 0; u < LUT_CH; ++u) {
+        if (c0 + u >= chunks) break;
+        float w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t sh = (k == 0 ? (b[u] << 2) : (b[u] >> (4 * k - 2)));
+          uint32_t addr;
+          asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(addr) : "r"(sh), "r"(0x3Cu), "r"(tsh));  // (sh & 0x3C) | tsh
+          // (memory clobber: ordered after this row's table store and before the next one's)
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(w[k]) : "r"(addr) : "memory");
+        }
+#pragma unroll
+        for (int t = 0; t < PT; ++t) {
+          const float4* xp = reinterpret_cast<const float4*>(sXf + t * n + 256 * (c0 + u) + 8 * lane);
+          const float4 x0 = xp[0], x1 = xp[1];
+          acc[t] = fmaf(w[0], x0.x, acc[t]);
+          acc[t] = fmaf(w[1], x0.y, acc[t]);
+          acc[t] = fmaf(w[2], x0.z, acc[t]);
+          acc[t] = fmaf(w[3], x0.w, acc[t]);
+          acc[t] = fmaf(w[4], x1.x, acc[t]);
+          acc[t] = fmaf(w[5], x1.y, acc[t]);
+          acc[t] = fmaf(w[6], x1.z, acc[t]);
+          acc[t] = fmaf(w[7], x1.w, acc[t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < PT; ++t)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < PT; ++t)
+        if (t < p) Y[(int64_t)t * m + row] = acc[t];
+    }
+    __syncwarp();
+  }
+}
+
+template <int PT>
+ganq_status_t launch_lut4_t(const uint8_t* P, const __half* T16, const __half* X, int64_t m, int64_t n, int64_t p,
+                            float* Y, cudaStream_t st) {
+  const size_t smem = (size_t)PT * n * sizeof(float);
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(lut4_gemm_kernel<PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lut4_gemm_kernel<PT>, 32 * LUT_WARPS, smem);
+  static const int cap = getenv("GANQ_LUT_CTAS_PER_SM") ? atoi(getenv("GANQ_LUT_CTAS_PER_SM")) : 0;
+  if (cap > 0 && cap < per_sm) per_sm = cap;
+  const int64_t want = (m + LUT_WARPS - 1) / LUT_WARPS;
+  const unsigned grid = (unsigned)min(want, (int64_t)sms * (per_sm > 0 ? per_sm : 1));
+  lut4_gemm_kernel<PT><<<grid, 32 * LUT_WARPS, smem, st>>>(P, T16, X, (int)m, (int)n, (int)p, Y);  // persistent
+  GANQ_LAUNCH_CHECK("lut4_gemm_kernel");
+  return GANQ_OK;
+}
+
 template <int N, int PT>
 ganq_status_t launch_lut_t(const uint8_t* P, const __half* T16, const __half* X, int64_t m, int64_t n, int64_t p,
                            float* Y, cudaStream_t st) {
   const int64_t npad = (n + 255) / 256 * 256;
-  const size_t smem = (size_t)LUT_WARPS * (1 << N) * sizeof(float) + (size_t)PT * npad * sizeof(__half);
+  const size_t smem = (size_t)LUT_WARPS * (1 << N) * sizeof(float) + (PT > 1 ? (size_t)PT * npad * sizeof(__half) : 0);
   if (smem > 227 * 1024) {
     set_error(GANQ_ERR_UNSUPPORTED, "lut_gemm: n = %lld too large for the shared-memory staging of X",
               (long long)n);
@@ -137,11 +295,22 @@ ganq_status_t launch_lut_t(const uint8_t* P, const __half* T16, const __half* X,
 template <int N>
 ganq_status_t launch_lut_n(const uint8_t* P, const __half* T16, const __half* X, int64_t m, int64_t n, int64_t p,
                            float* Y, cudaStream_t st) {
+  const bool fast = N == 4 && n % 256 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(P) & 3) == 0 && m < (1ll << 31) && n * LUT_PMAX < (1ll << 31) &&
+                    (size_t)LUT_PMAX * n * sizeof(float) <= 200 * 1024;
   for (int64_t t0 = 0; t0 < p; t0 += LUT_PMAX) {
     const int64_t pb = min((int64_t)LUT_PMAX, p - t0);
     ganq_status_t s;
     const __half* Xb = X + t0 * n;
     float* Yb = Y + t0 * m;
+    if (fast) {
+      if (pb == 1) s = launch_lut4_t<1>(P, T16, Xb, m, n, pb, Yb, st);
+      else if (pb == 2) s = launch_lut4_t<2>(P, T16, Xb, m, n, pb, Yb, st);
+      else if (pb <= 4) s = launch_lut4_t<4>(P, T16, Xb, m, n, pb, Yb, st);
+      else s = launch_lut4_t<8>(P, T16, Xb, m, n, pb, Yb, st);
+      if (s) return s;
+      continue;
+    }
     if (pb == 1) s = launch_lut_t<N, 1>(P, T16, Xb, m, n, pb, Yb, st);
     else if (pb == 2) s = launch_lut_t<N, 2>(P, T16, Xb, m, n, pb, Yb, st);
     else if (pb <= 4) s = launch_lut_t<N, 4>(P, T16, Xb, m, n, pb, Yb, st);
