@@ -252,6 +252,137 @@ lut4_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, 
   }
 }
 
+// Fast path for any N and n a multiple of 256: a chunk of 256 codes is 32 N bytes = 8 N words;
+// lanes < 8 N load one word each (coalesced), then every lane gathers its 8 N-bit window (codes
+// [8 l, 8 l + 8) of the chunk) with shuffles and a funnel shift.  Lookup and summation as in
+// lut4_gemm_kernel (same order: a lane's codes ascending, fmaf in fp32, then the butterfly).
+template <int N, int PT>
+__global__ void __launch_bounds__(32 * LUT_WARPS)
+lutn_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, const __half* __restrict__ X,
+                 int m, int n, int p, float* __restrict__ Y) {
+  constexpr int NL = 1 << N;
+  constexpr int WPC = 8 * N;  // words per chunk
+  __shared__ __align__(1024) float sT[LUT_WARPS * NL];
+  extern __shared__ __align__(16) float sXf[];  // [PT][n] fp32
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunks = n >> 8;
+  const int64_t rbw = (int64_t)n * N / 32;  // row length in words (n % 256 == 0)
+  uint32_t wn[2][LUT_CH];                    // prefetched words (lanes < WPC; two per lane if N > 4)
+  auto prefetch = [&](int r) {
+    const uint32_t* pr = reinterpret_cast<const uint32_t*>(P) + (int64_t)r * rbw;
+#pragma unroll
+    for (int u = 0; u < LUT_CH; ++u) {
+      wn[0][u] = (u < chunks && lane < WPC) ? __ldg(pr + WPC * u + lane) : 0u;
+      wn[1][u] = (N > 4 && u < chunks && lane + 32 < WPC) ? __ldg(pr + WPC * u + lane + 32) : 0u;
+    }
+  };
+  if (blockIdx.x * LUT_WARPS + warp < m) prefetch(blockIdx.x * LUT_WARPS + warp);
+  for (int e = threadIdx.x; e < PT * n / 8; e += blockDim.x) {
+    const int t = (8 * e) / n, j = (8 * e) % n;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (t < p) v = __ldg(reinterpret_cast<const uint4*>(X + (int64_t)t * n + j));
+    const __half2* h = reinterpret_cast<const __half2*>(&v);
+    float4 f0, f1;
+    f0.x = __low2float(h[0]); f0.y = __high2float(h[0]); f0.z = __low2float(h[1]); f0.w = __high2float(h[1]);
+    f1.x = __low2float(h[2]); f1.y = __high2float(h[2]); f1.z = __low2float(h[3]); f1.w = __high2float(h[3]);
+    reinterpret_cast<float4*>(sXf + 8 * e)[0] = f0;
+    reinterpret_cast<float4*>(sXf + 8 * e)[1] = f1;
+  }
+  __syncthreads();
+  const uint32_t tsh = smem_u32(sT) + (uint32_t)(warp * NL * 4);  // aligned to NL * 4 bytes
+  const int bit0 = 8 * N * lane;                                  // first bit of this lane in a chunk
+  const int wsrc = bit0 >> 5, sh0 = bit0 & 31;
+  const int stride = gridDim.x * LUT_WARPS;
+  for (int row = blockIdx.x * LUT_WARPS + warp; row < m; row += stride) {
+    uint32_t w0[LUT_CH], w1[LUT_CH];
+#pragma unroll
+    for (int u = 0; u < LUT_CH; ++u) { w0[u] = wn[0][u]; w1[u] = wn[1][u]; }
+    for (int e = lane; e < NL; e += 32) sT[warp * NL + e] = __half2float(T16[(int64_t)row * NL + e]);
+    if (row + stride < m) prefetch(row + stride);
+    __syncwarp();
+    const uint32_t* prow = reinterpret_cast<const uint32_t*>(P) + (int64_t)row * rbw;
+    float acc[PT];
+#pragma unroll
+    for (int t = 0; t < PT; ++t) acc[t] = 0.0f;
+    for (int c0 = 0; c0 < chunks; c0 += LUT_CH) {
+      uint32_t a0[LUT_CH], a1[LUT_CH];
+#pragma unroll
+      for (int u = 0; u < LUT_CH; ++u) {
+        const bool in = c0 + u < chunks;
+        a0[u] = (c0 == 0) ? w0[u] : ((in && lane < WPC) ? __ldg(prow + WPC * (c0 + u) + lane) : 0u);
+        a1[u] = (c0 == 0) ? w1[u] : ((N > 4 && in && lane + 32 < WPC) ? __ldg(prow + WPC * (c0 + u) + lane + 32) : 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < LUT_CH; ++u) {
+        if (c0 + u >= chunks) break;
+        // gather words wsrc, wsrc + 1, wsrc + 2 of the chunk (word q lives in lane q % 32, set q / 32)
+        auto word = [&](int q) {
+          const uint32_t lo = __shfl_sync(0xffffffffu, a0[u], q & 31);
+          if constexpr (N > 4) {
+            const uint32_t hi = __shfl_sync(0xffffffffu, a1[u], q & 31);
+            return q < 32 ? lo : hi;
+          }
+          return lo;
+        };
+        const uint32_t x0 = word(wsrc), x1 = word(wsrc + 1);
+        uint64_t bits = (((uint64_t)x1 << 32) | x0) >> sh0;
+        if constexpr (N > 4) {  // the shuffle runs in every lane (full-mask), the select afterwards
+          const uint64_t x2 = word(wsrc + 2);
+          bits |= (sh0 > 0) ? (x2 << (64 - sh0)) : 0ull;
+        }
+        float w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          // (code k) * 4 sits at bits [N k - 2, ...): shift right by N k - 2, or left when N k < 2
+          const uint32_t shv = (N * k >= 2) ? (uint32_t)(bits >> (N * k - 2)) : (uint32_t)(bits << (2 - N * k));
+          uint32_t addr;
+          asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(addr) : "r"(shv), "r"((uint32_t)(NL - 1) << 2), "r"(tsh));
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(w[k]) : "r"(addr) : "memory");
+        }
+#pragma unroll
+        for (int t = 0; t < PT; ++t) {
+          const float4* xp = reinterpret_cast<const float4*>(sXf + t * n + 256 * (c0 + u) + 8 * lane);
+          const float4 xa = xp[0], xb = xp[1];
+          acc[t] = fmaf(w[0], xa.x, acc[t]);
+          acc[t] = fmaf(w[1], xa.y, acc[t]);
+          acc[t] = fmaf(w[2], xa.z, acc[t]);
+          acc[t] = fmaf(w[3], xa.w, acc[t]);
+          acc[t] = fmaf(w[4], xb.x, acc[t]);
+          acc[t] = fmaf(w[5], xb.y, acc[t]);
+          acc[t] = fmaf(w[6], xb.z, acc[t]);
+          acc[t] = fmaf(w[7], xb.w, acc[t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < PT; ++t)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < PT; ++t)
+        if (t < p) Y[(int64_t)t * m + row] = acc[t];
+    }
+    __syncwarp();
+  }
+}
+
+template <int N, int PT>
+ganq_status_t launch_lutn_t(const uint8_t* P, const __half* T16, const __half* X, int64_t m, int64_t n, int64_t p,
+                            float* Y, cudaStream_t st) {
+  const size_t smem = (size_t)PT * n * sizeof(float);
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(lutn_gemm_kernel<N, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lutn_gemm_kernel<N, PT>, 32 * LUT_WARPS, smem);
+  const int64_t want = (m + LUT_WARPS - 1) / LUT_WARPS;
+  const unsigned grid = (unsigned)min(want, (int64_t)sms * (per_sm > 0 ? per_sm : 1));
+  lutn_gemm_kernel<N, PT><<<grid, 32 * LUT_WARPS, smem, st>>>(P, T16, X, (int)m, (int)n, (int)p, Y);  // persistent
+  GANQ_LAUNCH_CHECK("lutn_gemm_kernel");
+  return GANQ_OK;
+}
+
 template <int PT>
 ganq_status_t launch_lut4_t(const uint8_t* P, const __half* T16, const __half* X, int64_t m, int64_t n, int64_t p,
                             float* Y, cudaStream_t st) {
@@ -295,11 +426,15 @@ ganq_status_t launch_lut_t(const uint8_t* P, const __half* T16, const __half* X,
 template <int N>
 ganq_status_t launch_lut_n(const uint8_t* P, const __half* T16, const __half* X, int64_t m, int64_t n, int64_t p,
                            float* Y, cudaStream_t st) {
-  const bool fast = N == 4 && n % 256 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(P) & 3) == 0 && m < (1ll << 31) && n * LUT_PMAX < (1ll << 31) &&
-                    (size_t)LUT_PMAX * n * sizeof(float) <= 200 * 1024;
+  // whole chunks (n % 256 == 0: 32 N-byte chunks, word-aligned packed rows), 16-byte aligned X,
+  // and X of the batch (fp32) within shared memory
+  const bool whole = n % 256 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(P) & 3) == 0 && m < (1ll << 31) && n * LUT_PMAX < (1ll << 31);
   for (int64_t t0 = 0; t0 < p; t0 += LUT_PMAX) {
     const int64_t pb = min((int64_t)LUT_PMAX, p - t0);
+    const int64_t ptile = pb == 1 ? 1 : pb == 2 ? 2 : pb <= 4 ? 4 : 8;
+    const bool fits = (size_t)ptile * n * sizeof(float) <= 200 * 1024;
+    const bool fast = N == 4 && whole && fits, fastn = N != 4 && whole && fits;
     ganq_status_t s;
     const __half* Xb = X + t0 * n;
     float* Yb = Y + t0 * m;
@@ -308,6 +443,14 @@ ganq_status_t launch_lut_n(const uint8_t* P, const __half* T16, const __half* X,
       else if (pb == 2) s = launch_lut4_t<2>(P, T16, Xb, m, n, pb, Yb, st);
       else if (pb <= 4) s = launch_lut4_t<4>(P, T16, Xb, m, n, pb, Yb, st);
       else s = launch_lut4_t<8>(P, T16, Xb, m, n, pb, Yb, st);
+      if (s) return s;
+      continue;
+    }
+    if (fastn) {
+      if (pb == 1) s = launch_lutn_t<N, 1>(P, T16, Xb, m, n, pb, Yb, st);
+      else if (pb == 2) s = launch_lutn_t<N, 2>(P, T16, Xb, m, n, pb, Yb, st);
+      else if (pb <= 4) s = launch_lutn_t<N, 4>(P, T16, Xb, m, n, pb, Yb, st);
+      else s = launch_lutn_t<N, 8>(P, T16, Xb, m, n, pb, Yb, st);
       if (s) return s;
       continue;
     }

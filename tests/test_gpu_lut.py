@@ -54,8 +54,12 @@ def test_codebook_f16_bitwise():
     assert np.array_equal(T16.cpu().numpy().view(np.uint16), T.numpy().astype(np.float16).view(np.uint16))
 
 
-@pytest.mark.parametrize("m,n,p,nbits", [(64, 4096, 1, 4), (100, 300, 3, 3), (33, 131, 8, 2),
-                                         (17, 1000, 12, 8), (40, 256, 5, 1), (9, 520, 2, 5)])
+@pytest.mark.parametrize("m,n,p,nbits", [
+    # generic kernel (n not a multiple of 256)
+    (100, 300, 3, 3), (33, 131, 8, 2), (17, 1000, 12, 8), (9, 520, 2, 5),
+    # fast paths: N = 4 (direct words) and every other N (shuffled windows), n % 256 == 0
+    (64, 4096, 1, 4), (40, 256, 5, 1), (64, 4096, 1, 3), (32, 512, 3, 5), (16, 768, 9, 8),
+    (8, 256, 1, 2), (24, 1024, 4, 6), (10, 512, 2, 7), (300, 11008, 1, 3)])
 def test_lut_gemm_parity(m, n, p, nbits):
     rng = np.random.default_rng(m * 7 + n + p)
     Qn = rng.integers(0, 2 ** nbits, size=(m, n), dtype=np.uint8)
