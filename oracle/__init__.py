@@ -65,6 +65,12 @@ def _load():
         lib.or_lut_gemm.restype = None
         lib.or_storage_bytes.argtypes = [I64, I64, ctypes.c_int, ctypes.c_int]
         lib.or_storage_bytes.restype = ctypes.c_double
+        lib.or_outlier_indices.argtypes = [I64, ctypes.c_double, P, P]
+        lib.or_outlier_indices.restype = None
+        lib.or_outlier_split.argtypes = [P, I64, I64, ctypes.c_double, P, P, P, P]
+        lib.or_outlier_split.restype = None
+        lib.or_sparse_matmul.argtypes = [P, P, P, I64, I64, P, I64, P]
+        lib.or_sparse_matmul.restype = None
         lib.or_init_codebook.argtypes = [P, I64, I64, ctypes.c_int, P]
         lib.or_init_codebook.restype = None
         lib.or_sstep.argtypes = [P, P, P, I64, I64, ctypes.c_int, P, P]
@@ -254,3 +260,47 @@ STORAGE = {"fp16": 0, "uniform": 1, "lut": 2}
 def storage_bytes(m: int, n: int, nbits: int, scheme: str) -> float:
     """Table 1: fp16 2mn; uniform mnN/8 + 4m; LUT mnN/8 + 2*2^N*m."""
     return _load().or_storage_bytes(m, n, nbits, STORAGE[scheme])
+
+
+# --------------------------------------------------------------------------- NEXT-2
+def outlier_indices(n: int, r: float):
+    """(upper, lower): Algorithm 2's cutoff indices into the sorted row, 0-based."""
+    up, lo = ctypes.c_int64(), ctypes.c_int64()
+    _load().or_outlier_indices(n, r, ctypes.byref(up), ctypes.byref(lo))
+    return up.value, lo.value
+
+
+def outlier_split(W, r: float):
+    """Algorithm 2: returns (mask uint8, W_dense fp32, c_lower, c_upper) per row."""
+    lib = _load()
+    W = np.ascontiguousarray(W, dtype=np.float32)
+    m, n = W.shape
+    M = np.zeros((m, n), np.uint8)
+    Wd = np.zeros((m, n), np.float32)
+    clo = np.zeros(m, np.float32)
+    chi = np.zeros(m, np.float32)
+    lib.or_outlier_split(W.ctypes.data, m, n, r, M.ctypes.data, Wd.ctypes.data, clo.ctypes.data, chi.ctypes.data)
+    return M, Wd, clo, chi
+
+
+def csr_of(W, M):
+    """CSR (offsets int64, columns int32 ascending, values fp32) of W o M (the mask's entries)."""
+    m, n = W.shape
+    counts = M.sum(axis=1).astype(np.int64)
+    off = np.zeros(m + 1, np.int64)
+    off[1:] = np.cumsum(counts)
+    rows, cols = np.nonzero(M)
+    return off, cols.astype(np.int32), W[rows, cols].astype(np.float32)
+
+
+def sparse_matmul(off, col, val, m: int, n: int, X) -> np.ndarray:
+    """Y (p x m, fp64) = X W_sparse^T (the sparse path of GANQ*)."""
+    lib = _load()
+    off = np.ascontiguousarray(off, np.int64)
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float32)
+    X = np.ascontiguousarray(X, np.float64)
+    p = X.shape[0]
+    Y = np.zeros((p, m), np.float64)
+    lib.or_sparse_matmul(off.ctypes.data, col.ctypes.data, val.ctypes.data, m, n, X.ctypes.data, p, Y.ctypes.data)
+    return Y

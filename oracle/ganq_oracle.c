@@ -514,3 +514,61 @@ double or_storage_bytes(int64_t m, int64_t n, int N, int scheme) {
     if (scheme == 1) return q + 4.0 * (double)m;
     return q + 2.0 * (double)(1 << N) * (double)m;
 }
+
+/* ========================================================================= */
+/* NEXT-2: GANQ* outlier extraction, Algorithm 2 (Appendix B).    */
+/* ========================================================================= */
+
+/* Cutoff indices of Algorithm 2 into the ascending-sorted row (0-based, reading R-21):
+ *   p = 1 - 0.5 r;  upper = floor(n p);  lower = ceil(n (1 - p)). */
+void or_outlier_indices(int64_t n, double r, int64_t *upper, int64_t *lower) {
+    const double p = 1.0 - 0.5 * r;
+    *upper = (int64_t)floor((double)n * p);
+    *lower = (int64_t)ceil((double)n * (1.0 - p));
+}
+
+static int cmp_float(const void *a, const void *b) {
+    const float x = *(const float *)a, y = *(const float *)b;
+    return (x < y) ? -1 : (x > y) ? 1 : 0;
+}
+
+/* Algorithm 2, row by row: sort, c_upper = sorted[upper], c_lower = sorted[lower],
+ * O = (W >= c_upper) | (W <= c_lower), W_sparse = W o M, W_dense = W - W_sparse.
+ * Outputs: mask M (m x n bytes), W_dense (m x n), the two cutoffs per row. */
+void or_outlier_split(const float *W, int64_t m, int64_t n, double r, uint8_t *M, float *Wd,
+                      float *c_lo, float *c_hi) {
+    int64_t up, lo;
+    or_outlier_indices(n, r, &up, &lo);
+#pragma omp parallel
+    {
+        float *srt = (float *)malloc(sizeof(float) * (size_t)n);
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < m; ++i) {
+            memcpy(srt, W + i * n, sizeof(float) * (size_t)n);
+            qsort(srt, (size_t)n, sizeof(float), cmp_float);
+            const float cu = srt[up], cl = srt[lo];
+            c_hi[i] = cu;
+            c_lo[i] = cl;
+            for (int64_t j = 0; j < n; ++j) {
+                const float w = W[i * n + j];
+                const int o = (w >= cu) || (w <= cl);
+                M[i * n + j] = (uint8_t)o;
+                const float ws = o ? w : 0.0f;          /* W o M */
+                Wd[i * n + j] = w - ws;                  /* W - W_sparse (exact) */
+            }
+        }
+        free(srt);
+    }
+}
+
+/* Y (p x m) = X W_sparse^T, fp64, from a CSR (row offsets, column indices, values). */
+void or_sparse_matmul(const int64_t *off, const int32_t *col, const float *val, int64_t m, int64_t n,
+                      const double *X, int64_t p, double *Y) {
+    (void)n;
+    for (int64_t t = 0; t < p; ++t)
+        for (int64_t i = 0; i < m; ++i) {
+            double acc = 0.0;
+            for (int64_t k = off[i]; k < off[i + 1]; ++k) acc += (double)val[k] * X[t * n + col[k]];
+            Y[t * m + i] = acc;
+        }
+}
