@@ -300,6 +300,7 @@ def run_ours(args):
     lut = None
     if rank == 0 and not args.no_lut:
         lut = lut_gemv_bench(g, Q, T, ml, n, nbits, peaks, dev)
+        lut["outlier_split"] = outlier_bench(g, Wl, peaks)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -328,6 +329,26 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def outlier_bench(g, W, peaks, reps=20, r=0.005):
+    """NEXT-2: GANQ* split of the layer's W (Algorithm 2, r = 0.5 %), device time of the
+    split + CSR kernels; algorithmic bytes = read W + write W_dense (+ the CSR)."""
+    Wd, (off, col, val), _ = g.outlier_split(W, r)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.outlier_split(W, r)  # (synchronises once per call for the host nnz)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / reps * 1e3
+    nbytes = 2 * W.numel() * 4 + off.numel() * 8 + col.numel() * 8
+    ach = nbytes / (us * 1e-6) / 1e9
+    return {"us": round(us, 1), "nnz": int(col.numel()), "nnz_frac": round(col.numel() / W.numel(), 5),
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(ach / peaks["hbm_gbs"], 4)},
+            "note": "includes the host synchronisation for nnz between the two kernels"}
 
 
 def lut_gemv_bench(g, Q, T, m, n, nbits, peaks, dev, reps=200):

@@ -192,6 +192,30 @@ ganq_status_t ganq_codebook_f16(const float* T, int64_t m, int n_bits, uint16_t*
 ganq_status_t ganq_lut_gemm(const uint8_t* packed, const uint16_t* T16, const uint16_t* X, int64_t m,
                             int64_t n, int64_t p, int n_bits, float* Y, void* stream);
 
+/*
+ * ---------------------------------------------------------------- NEXT-2: GANQ* outlier split
+ * Algorithm 2 (Appendix B; §3.3).  Per row, with p = 1 - 0.5 r, the
+ * cutoffs are the row's ascending order statistics at 0-based indices floor(n p) (c_upper) and
+ * ceil(n (1 - p)) (c_lower); an entry is an outlier iff w >= c_upper or w <= c_lower (ties
+ * included).  W_sparse = W o M, W_dense = W - W_sparse (exact).  GANQ* quantizes W_dense; its
+ * objective is ganq_objective(W_dense, Q, T, H) since W - (W~_dense + W_sparse) = W_dense - W~_dense.
+ *
+ * ganq_outlier_split: W (m x n fp32) -> W_dense (m x n), per-row cutoffs c_lower / c_upper (m),
+ * CSR row offsets (m + 1 int64) of W_sparse, and its nnz (HOST; synchronises the stream).
+ * INVALID_ARG: m < 1, n < 2, r not in (0, 1), null pointers; UNSUPPORTED: n > 57344 (one row of
+ * keys must fit in shared memory).
+ * ganq_outlier_csr: fills col_idx (int32, ascending within a row) and values (fp32) of W_sparse
+ * (nnz entries, as returned above).  Async.
+ * ganq_sparse_gemm_add: Y (p x m fp32) += X W_sparse^T, X p x n fp16 -- the sparse path of the
+ * deployed GANQ* layer next to ganq_lut_gemm.  Async.
+ */
+ganq_status_t ganq_outlier_split(const float* W, int64_t m, int64_t n, double r, float* W_dense, float* c_lower,
+                                 float* c_upper, int64_t* row_offsets, int64_t* nnz, void* stream);
+ganq_status_t ganq_outlier_csr(const float* W, int64_t m, int64_t n, const float* c_lower, const float* c_upper,
+                               const int64_t* row_offsets, int32_t* col_idx, float* values, void* stream);
+ganq_status_t ganq_sparse_gemm_add(const int64_t* row_offsets, const int32_t* col_idx, const float* values,
+                                   int64_t m, int64_t n, const uint16_t* X, int64_t p, float* Y, void* stream);
+
 const char* ganq_version(void);
 
 #ifdef __cplusplus

@@ -8,11 +8,13 @@ Public API (torch CUDA tensors; thin binding of include/ganq.h):
     factor(H)                          L = chol(H')          Eq. (9) + App. A
     dist.quantize_layer_distributed    token-sharded H + row-sharded solve over NCCL
     pack_codes / codebook_f16 / lut_gemm   NEXT-1: N-bit storage and LUT mpGEMM (Fig. 1a)
+    outlier_split / sparse_gemm_add        NEXT-2: GANQ* decomposition (Algorithm 2)
 """
-from .api import (codebook_f16, factor, hessian, lut_gemm, objective, objective_workspace_size,
-                  pack_codes, quantize_layer, tstep, version, workspace_size)
+from .api import (codebook_f16, factor, hessian, lut_gemm, objective, objective_workspace_size, outlier_split,
+                  pack_codes, quantize_layer, sparse_gemm_add, tstep, version, workspace_size)
 from ._lib import GanqError, NotPositiveDefinite
 
 __all__ = ["hessian", "quantize_layer", "objective", "tstep", "factor", "workspace_size",
-           "objective_workspace_size", "version", "pack_codes", "codebook_f16", "lut_gemm", "GanqError",
+           "objective_workspace_size", "version", "pack_codes", "codebook_f16", "lut_gemm", "outlier_split",
+           "sparse_gemm_add", "GanqError",
            "NotPositiveDefinite"]

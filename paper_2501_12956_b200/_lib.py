@@ -43,6 +43,9 @@ SIG = {
     "ganq_pack_codes": (I32, [P, I64, I64, I32, P, P]),
     "ganq_codebook_f16": (I32, [P, I64, I32, P, P]),
     "ganq_lut_gemm": (I32, [P, P, P, I64, I64, I64, I32, P, P]),
+    "ganq_outlier_split": (I32, [P, I64, I64, ctypes.c_double, P, P, P, P, P, P]),
+    "ganq_outlier_csr": (I32, [P, I64, I64, P, P, P, P, P, P]),
+    "ganq_sparse_gemm_add": (I32, [P, P, P, I64, I64, P, I64, P, P]),
 }
 
 

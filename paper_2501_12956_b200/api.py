@@ -14,7 +14,8 @@ import torch
 from . import _lib
 
 __all__ = ["hessian", "quantize_layer", "objective", "tstep", "factor", "workspace_size",
-           "objective_workspace_size", "version", "pack_codes", "codebook_f16", "lut_gemm"]
+           "objective_workspace_size", "version", "pack_codes", "codebook_f16", "lut_gemm", "outlier_split",
+           "sparse_gemm_add"]
 
 
 def _ptr(t):
@@ -207,4 +208,39 @@ def lut_gemm(P, T16, X, n: int, Y=None, stream=None):
     if Y is None:
         Y = torch.empty((p, m), dtype=torch.float32, device=X.device)
     _lib.check(_lib.load().ganq_lut_gemm(_ptr(P), _ptr(T16), _ptr(X), m, n, p, n_bits, _ptr(Y), _stream(stream)))
+    return Y
+
+
+# --------------------------------------------------------------------------- NEXT-2
+def outlier_split(W, r: float, stream=None):
+    """GANQ* decomposition, Algorithm 2: returns (W_dense, csr, cutoffs) with
+    csr = (row_offsets int64 m+1, col_idx int32, values fp32) of W_sparse and cutoffs =
+    (c_lower, c_upper) per row."""
+    _need(W, torch.float32, 2, "W")
+    m, n = W.shape
+    dev = W.device
+    Wd = torch.empty_like(W)
+    clo = torch.empty(m, dtype=torch.float32, device=dev)
+    chi = torch.empty(m, dtype=torch.float32, device=dev)
+    off = torch.empty(m + 1, dtype=torch.int64, device=dev)
+    nnz = ctypes.c_int64(0)
+    lib = _lib.load()
+    _lib.check(lib.ganq_outlier_split(_ptr(W), m, n, float(r), _ptr(Wd), _ptr(clo), _ptr(chi), _ptr(off),
+                                      ctypes.byref(nnz), _stream(stream)))
+    col = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)[: nnz.value]
+    val = torch.empty(max(nnz.value, 1), dtype=torch.float32, device=dev)[: nnz.value]
+    _lib.check(lib.ganq_outlier_csr(_ptr(W), m, n, _ptr(clo), _ptr(chi), _ptr(off), _ptr(col), _ptr(val),
+                                    _stream(stream)))
+    return Wd, (off, col, val), (clo, chi)
+
+
+def sparse_gemm_add(csr, X, Y, stream=None):
+    """Y (p x m fp32) += X W_sparse^T for the CSR of outlier_split; X: p x n fp16."""
+    off, col, val = csr
+    _need(X, torch.float16, 2, "X")
+    _need(Y, torch.float32, 2, "Y")
+    m = off.numel() - 1
+    p, n = X.shape
+    _lib.check(_lib.load().ganq_sparse_gemm_add(_ptr(off), _ptr(col), _ptr(val), m, n, _ptr(X), p, _ptr(Y),
+                                                _stream(stream)))
     return Y

@@ -303,6 +303,48 @@ ganq_status_t ganq_lut_gemm(const uint8_t* packed, const uint16_t* T16, const ui
   return launch_lut_gemm(packed, T16, X, m, n, p, n_bits, Y, (cudaStream_t)stream);
 }
 
+ganq_status_t ganq_outlier_split(const float* W, int64_t m, int64_t n, double r, float* W_dense, float* c_lower,
+                                 float* c_upper, int64_t* row_offsets, int64_t* nnz, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (m < 1 || n < 2 || !(r > 0.0 && r < 1.0) || !W || !W_dense || !c_lower || !c_upper || !row_offsets || !nnz) {
+    set_error(GANQ_ERR_INVALID_ARG, "outlier_split: need m >= 1, n >= 2, 0 < r < 1, non-null buffers");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  if (n > 57344) {
+    set_error(GANQ_ERR_UNSUPPORTED, "outlier_split: n = %lld exceeds the shared-memory row (57344)", (long long)n);
+    return GANQ_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  ganq_status_t s = launch_outlier_split(W, m, n, r, W_dense, c_lower, c_upper, row_offsets, st);
+  if (s) return s;
+  GANQ_CUDA_TRY(cudaMemcpyAsync(nnz, row_offsets + m, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GANQ_CUDA_TRY(cudaStreamSynchronize(st));
+  return GANQ_OK;
+}
+
+ganq_status_t ganq_outlier_csr(const float* W, int64_t m, int64_t n, const float* c_lower, const float* c_upper,
+                               const int64_t* row_offsets, int32_t* col_idx, float* values, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (m < 1 || n < 1 || !W || !c_lower || !c_upper || !row_offsets || !col_idx || !values) {
+    set_error(GANQ_ERR_INVALID_ARG, "outlier_csr: need m, n >= 1, non-null buffers");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  return launch_outlier_csr(W, m, n, c_lower, c_upper, row_offsets, col_idx, values, (cudaStream_t)stream);
+}
+
+ganq_status_t ganq_sparse_gemm_add(const int64_t* row_offsets, const int32_t* col_idx, const float* values,
+                                   int64_t m, int64_t n, const uint16_t* X, int64_t p, float* Y, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (m < 1 || n < 1 || p < 1 || !row_offsets || !X || !Y) {
+    set_error(GANQ_ERR_INVALID_ARG, "sparse_gemm_add: need m, n, p >= 1, non-null buffers");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  return launch_sparse_gemm_add(row_offsets, col_idx, values, m, n, X, p, Y, (cudaStream_t)stream);
+}
+
 const char* ganq_version(void) { return "ganq-b200 0.1 (sm_100a)"; }
 
 ganq_status_t ganq_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate,

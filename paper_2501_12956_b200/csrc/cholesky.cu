@@ -5,9 +5,9 @@
 // Factorisation: right-looking blocked Cholesky with NB = 64, in place on the lower
 // triangle of A (fp64).  Per block column k: (1) one CTA factors the 64 x 64 diagonal
 // block in shared memory, (2) TRSM of the panel below it (thread per row, forward
-// substitution from shared memory), (3) trailing SYRK update of the lower tiles (128 x 128 tiles,
-// 8 x 8 fp64 register blocking, K = 64).  Each tile has one
-// owner per step, so the result is deterministic (bitwise identical on every rank).
+// substitution from shared memory), (3) trailing SYRK update of the lower tiles (128 x 128
+// tiles, 8 x 8 fp64 register blocking), applied once per two panels (K = 128).  Each tile has
+// one owner per step, so the result is deterministic (bitwise identical on every rank).
 // A non-positive pivot records its global index (atomicMin) in *d_status.
 #include <float.h>
 #include <limits.h>
@@ -191,37 +191,43 @@ __global__ void __launch_bounds__(TR) trsm_panel_kernel(double* __restrict__ A, 
 // A[i, j] -= sum_c L[i, k0+c] L[j, k0+c] for the lower 128 x 128 tiles of the trailing matrix;
 // thread (tx, ty) owns the 8 x 8 elements (ty + 16 x, tx + 16 y) of its tile.
 constexpr int ST = 128;  // SYRK tile
-__global__ void __launch_bounds__(256) syrk_trailing_kernel(double* __restrict__ A, int64_t n,
-                                                            int64_t k0) {
+// A[i, j] -= sum_{c in [k0, k0 + kw)} L[i, c] L[j, c] for base <= j <= i < n, j < cend: the lower
+// 128 x 128 tiles of the trailing block, the kw <= 128 panel columns streamed through shared
+// memory in chunks of 64 (the accumulators stay in registers, one read-modify-write per tile).
+__global__ void __launch_bounds__(256) syrk_trailing_kernel(double* __restrict__ A, int64_t n, int64_t k0,
+                                                            int kw, int64_t base, int64_t cend) {
   const int ti = blockIdx.y, tj = blockIdx.x;
   if (tj > ti) return;
   extern __shared__ double syrk_smem[];
   double* Pi = syrk_smem;
   double* Pj = syrk_smem + ST * LDS;
-  const int64_t base = k0 + NB;  // first trailing row/col (only called when k0 + NB < n)
   const int64_t i0 = base + (int64_t)ti * ST, j0 = base + (int64_t)tj * ST;
-  for (int e = threadIdx.x; e < ST * NB; e += 256) {
-    const int r = e >> 6, c = e & 63;
-    if (i0 + r < n) cp8(&Pi[r * LDS + c], &A[(i0 + r) * n + k0 + c]);
-    else Pi[r * LDS + c] = 0.0;
-    if (j0 + r < n) cp8(&Pj[r * LDS + c], &A[(j0 + r) * n + k0 + c]);
-    else Pj[r * LDS + c] = 0.0;
-  }
-  cp_wait();
-  __syncthreads();
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double acc[8][8] = {};
+  for (int kc = 0; kc < kw; kc += NB) {
+    const int kcw = min(NB, kw - kc);
+    if (kc > 0) __syncthreads();  // the previous chunk has been consumed
+    for (int e = threadIdx.x; e < ST * NB; e += 256) {
+      const int r = e >> 6, c = e & 63;
+      if (i0 + r < n && c < kcw) cp8(&Pi[r * LDS + c], &A[(i0 + r) * n + k0 + kc + c]);
+      else Pi[r * LDS + c] = 0.0;
+      if (j0 + r < cend && c < kcw) cp8(&Pj[r * LDS + c], &A[(j0 + r) * n + k0 + kc + c]);
+      else Pj[r * LDS + c] = 0.0;
+    }
+    cp_wait();
+    __syncthreads();
 #pragma unroll 2
-  for (int c = 0; c < NB; ++c) {
-    double a[8], b[8];
+    for (int c = 0; c < NB; ++c) {
+      double a[8], b[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = Pi[(ty + 16 * q) * LDS + c];
+      for (int q = 0; q < 8; ++q) a[q] = Pi[(ty + 16 * q) * LDS + c];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) b[q] = Pj[(tx + 16 * q) * LDS + c];
+      for (int q = 0; q < 8; ++q) b[q] = Pj[(tx + 16 * q) * LDS + c];
 #pragma unroll
-    for (int x = 0; x < 8; ++x)
+      for (int x = 0; x < 8; ++x)
 #pragma unroll
-      for (int y = 0; y < 8; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+        for (int y = 0; y < 8; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+    }
   }
   // read-modify-write in two batches of 32: all loads of a batch are issued before its stores
   // (the compiler keeps loads and stores through one pointer in order, one round trip each)
@@ -233,14 +239,14 @@ __global__ void __launch_bounds__(256) syrk_trailing_kernel(double* __restrict__
 #pragma unroll
       for (int y = 0; y < 8; ++y) {
         const int64_t i = i0 + ty + 16 * (4 * h + x), j = j0 + tx + 16 * y;
-        old[x][y] = (i < n && j <= i) ? A[i * n + j] : 0.0;
+        old[x][y] = (i < n && j <= i && j < cend) ? A[i * n + j] : 0.0;
       }
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 8; ++y) {
         const int64_t i = i0 + ty + 16 * (4 * h + x), j = j0 + tx + 16 * y;
-        if (i < n && j <= i) A[i * n + j] = old[x][y] - acc[4 * h + x][y];
+        if (i < n && j <= i && j < cend) A[i * n + j] = old[x][y] - acc[4 * h + x][y];
       }
   }
 }
@@ -288,16 +294,35 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t 
   GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
   GANQ_CUDA_TRY(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
-  for (int64_t k0 = 0; k0 < n; k0 += NB) {
+  // two panels per pass: factor panel k, update only panel k + 1's columns (thin SYRK), factor
+  // panel k + 1, then one trailing SYRK with both panels (K = 128): the trailing matrix is read
+  // and written once per 128 columns
+  auto panel = [&](int64_t k0) -> ganq_status_t {
     potrf_diag_kernel<<<1, 256, kPotrfSmem, st>>>(A, n, k0, d_status);
     GANQ_LAUNCH_CHECK("potrf_diag_kernel");
     const int64_t rest = n - k0 - NB;
-    if (rest <= 0) break;
-    trsm_panel_kernel<<<(unsigned)((rest + TR - 1) / TR), TR, kTrsmSmem, st>>>(A, n, k0);
-    GANQ_LAUNCH_CHECK("trsm_panel_kernel");
-    const unsigned T = (unsigned)((rest + ST - 1) / ST);
-    syrk_trailing_kernel<<<dim3(T, T), 256, kSyrkSmem, st>>>(A, n, k0);
+    if (rest > 0) {
+      trsm_panel_kernel<<<(unsigned)((rest + TR - 1) / TR), TR, kTrsmSmem, st>>>(A, n, k0);
+      GANQ_LAUNCH_CHECK("trsm_panel_kernel");
+    }
+    return GANQ_OK;
+  };
+  auto syrk = [&](int64_t k0, int kw, int64_t base, int64_t cend) -> ganq_status_t {
+    const unsigned Ti = (unsigned)((n - base + ST - 1) / ST), Tj = (unsigned)((cend - base + ST - 1) / ST);
+    syrk_trailing_kernel<<<dim3(Tj, Ti), 256, kSyrkSmem, st>>>(A, n, k0, kw, base, cend);
     GANQ_LAUNCH_CHECK("syrk_trailing_kernel");
+    return GANQ_OK;
+  };
+  for (int64_t k0 = 0; k0 < n; k0 += 2 * NB) {
+    ganq_status_t s;
+    if ((s = panel(k0))) return s;
+    const int64_t k1 = k0 + NB;
+    if (k1 >= n) break;
+    if ((s = syrk(k0, NB, k1, min(k1 + NB, n)))) return s;  // panel k+1's columns only
+    if ((s = panel(k1))) return s;
+    const int64_t base = k1 + NB;
+    if (base >= n) break;
+    if ((s = syrk(k0, 2 * NB, base, n))) return s;          // trailing block, both panels
   }
   zero_upper_kernel<<<1184, 256, 0, st>>>(A, n);
   GANQ_LAUNCH_CHECK("zero_upper_kernel");

@@ -53,6 +53,14 @@ ganq_status_t launch_pack_codes(const uint8_t* Q, int64_t m, int64_t n, int N, u
 ganq_status_t launch_codebook_f16(const float* T, int64_t total, uint16_t* T16, cudaStream_t st);
 ganq_status_t launch_lut_gemm(const uint8_t* P, const uint16_t* T16, const uint16_t* X, int64_t m, int64_t n,
                               int64_t p, int N, float* Y, cudaStream_t st);
+// outlier.cu (NEXT-2)
+void outlier_indices(int64_t n, double r, int64_t* up, int64_t* lo);
+ganq_status_t launch_outlier_split(const float* W, int64_t m, int64_t n, double r, float* Wd, float* c_lo,
+                                   float* c_hi, int64_t* off, cudaStream_t st);
+ganq_status_t launch_outlier_csr(const float* W, int64_t m, int64_t n, const float* c_lo, const float* c_hi,
+                                 const int64_t* off, int32_t* col, float* val, cudaStream_t st);
+ganq_status_t launch_sparse_gemm_add(const int64_t* off, const int32_t* col, const float* val, int64_t m, int64_t n,
+                                     const uint16_t* X, int64_t p, float* Y, cudaStream_t st);
 // tgram_tc.cu
 int64_t tq_pitch(int64_t n);
 ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* scale, cudaStream_t st);
