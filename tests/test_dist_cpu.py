@@ -80,7 +80,7 @@ def test_world2_gloo_matches_single_process():
     oracle.build()
     world = 2
     port = _free_port()
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.start_processes(_worker, args=(world, port, out), nprocs=world, start_method="spawn", join=True)
     m, n, p, nbits, K = 23, 40, 3 * HESSIAN_CHUNK // 64, 3, 3
