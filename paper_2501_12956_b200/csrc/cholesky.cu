@@ -294,9 +294,9 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t 
   GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
   GANQ_CUDA_TRY(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
-  // two panels per pass: factor panel k, update only panel k + 1's columns (thin SYRK), factor
-  // panel k + 1, then one trailing SYRK with both panels (K = 128): the trailing matrix is read
-  // and written once per 128 columns
+  // large n: two panels per pass -- factor panel k, update only panel k + 1's columns (thin
+  // SYRK), factor panel k + 1, then one trailing SYRK with both panels (K = 128): the trailing
+  // matrix (beyond L2) is read and written once per 128 columns
   auto panel = [&](int64_t k0) -> ganq_status_t {
     potrf_diag_kernel<<<1, 256, kPotrfSmem, st>>>(A, n, k0, d_status);
     GANQ_LAUNCH_CHECK("potrf_diag_kernel");
@@ -313,16 +313,26 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t 
     GANQ_LAUNCH_CHECK("syrk_trailing_kernel");
     return GANQ_OK;
   };
-  for (int64_t k0 = 0; k0 < n; k0 += 2 * NB) {
-    ganq_status_t s;
-    if ((s = panel(k0))) return s;
-    const int64_t k1 = k0 + NB;
-    if (k1 >= n) break;
-    if ((s = syrk(k0, NB, k1, min(k1 + NB, n)))) return s;  // panel k+1's columns only
-    if ((s = panel(k1))) return s;
-    const int64_t base = k1 + NB;
-    if (base >= n) break;
-    if ((s = syrk(k0, 2 * NB, base, n))) return s;          // trailing block, both panels
+  if (n < 6144) {
+    // the trailing matrix (<= 300 MB) largely stays in L2: one panel per pass (fewer launches)
+    for (int64_t k0 = 0; k0 < n; k0 += NB) {
+      ganq_status_t s;
+      if ((s = panel(k0))) return s;
+      if (k0 + NB >= n) break;
+      if ((s = syrk(k0, NB, k0 + NB, n))) return s;
+    }
+  } else {
+    for (int64_t k0 = 0; k0 < n; k0 += 2 * NB) {
+      ganq_status_t s;
+      if ((s = panel(k0))) return s;
+      const int64_t k1 = k0 + NB;
+      if (k1 >= n) break;
+      if ((s = syrk(k0, NB, k1, min(k1 + NB, n)))) return s;  // panel k+1's columns only
+      if ((s = panel(k1))) return s;
+      const int64_t base = k1 + NB;
+      if (base >= n) break;
+      if ((s = syrk(k0, 2 * NB, base, n))) return s;          // trailing block, both panels
+    }
   }
   zero_upper_kernel<<<1184, 256, 0, st>>>(A, n);
   GANQ_LAUNCH_CHECK("zero_upper_kernel");
