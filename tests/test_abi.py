@@ -106,3 +106,8 @@ def test_packed_row_bytes(lib):
     assert lib.ganq_packed_row_bytes(4096, 4) == 2048
     assert lib.ganq_packed_row_bytes(7, 3) == 3
     assert lib.ganq_packed_row_bytes(0, 4) == 0 and lib.ganq_packed_row_bytes(5, 9) == 0
+
+
+def test_pipeline_module_imports():
+    from paper_2501_12956_b200 import pipeline
+    assert hasattr(pipeline, "LayerPipeline") and hasattr(pipeline, "quantize_layers")
