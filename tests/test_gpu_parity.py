@@ -318,3 +318,34 @@ def test_c2_full_size_sampled_rows(nrows):
     # H property at full size: symmetric, PSD diagonal
     assert torch.equal(H, H.T)
     assert bool(torch.all(torch.diagonal(H) > 0))
+
+
+def test_c3_full_size_factor_and_sampled_rows():
+    """BASELINE config c3 (LLaMA-2-7B down_proj: m = 4096, n = 11008, 3-bit, p = 262144, K = 10),
+    the two-panel Cholesky path (n >= 6144) and 8 levels.  P-2 at full size against LAPACK's
+    Cholesky of the same H' (a library routine as the factor step: the C oracle's unblocked
+    factor takes minutes at n = 11008); then the oracle's S- and T-steps re-solve sampled rows
+    from that factor and raw H, and the per-row objectives must agree (free-running, R-13)."""
+    c = synthetic.CONFIGS["c3"]
+    m, n, p, nbits, K = c["m"], c["n"], c["p"], c["nbits"], c["iters"]
+    W = synthetic.make_weights(m, n, seed=1000, device=DEV)
+    X = synthetic.make_activations(p, n, seed=2000, device=DEV)
+    H = g.hessian(X)
+    del X
+    L, delta = g.factor(H, "adaptive")
+    Hn = H.cpu().numpy()
+    Lnp = np.linalg.cholesky(Hn + np.diag(delta.cpu().numpy()))
+    assert rel_fro(L.cpu().numpy(), Lnp) <= 1e-9
+    del L
+    Q, T = g.quantize_layer(W, H, nbits, K)
+    _, pr = g.objective(W, Q, T, H, per_row=True)
+    rows = np.linspace(0, m - 1, 4).astype(int)
+    Ws32 = W[rows].cpu().numpy()
+    Ws = Ws32.astype(np.float64)
+    To = oracle.init_codebook(Ws32, nbits).astype(np.float64)
+    for _ in range(K):
+        Qo, _ = oracle.sstep(Ws, Lnp, To)
+        To = oracle.tstep(Ws, Qo, Hn, 1 << nbits)
+    _, pro = oracle.objective(Ws, Qo, To, Hn, per_row=True)
+    np.testing.assert_allclose(pr.cpu().numpy()[rows], pro, rtol=1e-3)
+    assert float(np.mean(Q.cpu().numpy()[rows] == Qo)) > 0.9
