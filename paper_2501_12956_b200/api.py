@@ -95,7 +95,19 @@ def quantize_layer(W: torch.Tensor, H: torch.Tensor, n_bits: int, iters: int = 1
                    precond: str = "adaptive", lam: float = 0.0, tau: float = 1e-7,
                    T0: torch.Tensor | None = None, empty_level_rule: int = 0, trace: bool = False,
                    Q: torch.Tensor | None = None, T: torch.Tensor | None = None, stream=None):
-    """Algorithm 1 given H: returns (Q uint8 m x n, T fp32 m x 2^N[, obj_trace])."""
+    """Algorithm 1 given H: returns (Q uint8 m x n, T fp32 m x 2^N[, obj_trace]).
+
+    precond: "adaptive" (App. A, default), "fixed_lambda" (H + lam I, Remark 1), "none", or
+    "auto" (none, falling back to adaptive on a non-positive pivot)."""
+    if precond == "auto":
+        # NEXT-4 "on failure only": no preconditioning unless the factor hits a non-positive
+        # pivot, then the adaptive shift of App. A (P:460-467)
+        try:
+            return quantize_layer(W, H, n_bits, iters, precond="none", lam=lam, tau=tau, T0=T0,
+                                  empty_level_rule=empty_level_rule, trace=trace, Q=Q, T=T, stream=stream)
+        except _lib.NotPositiveDefinite:
+            return quantize_layer(W, H, n_bits, iters, precond="adaptive", lam=lam, tau=tau, T0=T0,
+                                  empty_level_rule=empty_level_rule, trace=trace, Q=Q, T=T, stream=stream)
     _need(W, torch.float32, 2, "W")
     _need(H, torch.float64, 2, "H")
     m, n = W.shape

@@ -349,3 +349,21 @@ def test_c3_full_size_factor_and_sampled_rows():
     _, pro = oracle.objective(Ws, Qo, To, Hn, per_row=True)
     np.testing.assert_allclose(pr.cpu().numpy()[rows], pro, rtol=1e-3)
     assert float(np.mean(Q.cpu().numpy()[rows] == Qo)) > 0.9
+
+
+def test_precond_auto_policy():
+    """NEXT-4 'on failure only': auto = none when H is positive definite, adaptive when the factor
+    meets a non-positive pivot (a dead channel)."""
+    W, X = make_case(16, 64, 400, seed=9)
+    H = gpu_H(X)
+    Qa, Ta = g.quantize_layer(W.to(DEV), H, 3, 2, precond="auto")
+    Qn, Tn = g.quantize_layer(W.to(DEV), H, 3, 2, precond="none")
+    assert torch.equal(Qa, Qn) and torch.equal(Ta, Tn)
+    X2 = X.clone()
+    X2[:, 11] = 0
+    H2 = gpu_H(X2)
+    with pytest.raises(g.NotPositiveDefinite):
+        g.quantize_layer(W.to(DEV), H2, 3, 2, precond="none")
+    Qa2, Ta2 = g.quantize_layer(W.to(DEV), H2, 3, 2, precond="auto")
+    Qd2, Td2 = g.quantize_layer(W.to(DEV), H2, 3, 2, precond="adaptive")
+    assert torch.equal(Qa2, Qd2) and torch.equal(Ta2, Td2)
