@@ -286,6 +286,29 @@ ganq_status_t launch_precondition(const double* H, int64_t n, int policy, double
   return GANQ_OK;
 }
 
+// Side stream and events of the Cholesky look-ahead, created once per host thread and device.
+struct LookAhead {
+  int device = -1;
+  cudaStream_t side = nullptr;
+  cudaEvent_t th = nullptr, tr = nullptr;
+};
+LookAhead& look_ahead() {
+  static thread_local LookAhead la;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (la.device != dev) {
+    // highest priority: the side stream's panel kernels take SMs as soon as bulk-update CTAs
+    // retire instead of queueing behind the bulk kernel's remaining CTAs
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&la.side, cudaStreamNonBlocking, hi);
+    cudaEventCreateWithFlags(&la.th, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&la.tr, cudaEventDisableTiming);
+    la.device = dev;
+  }
+  return la;
+}
+
 ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t st) {
   constexpr int kSyrkSmem = 2 * ST * LDS * sizeof(double);
   constexpr int kTrsmSmem = ((TR + NB) * LDS + NB) * sizeof(double);
@@ -294,15 +317,12 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t 
   GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
   GANQ_CUDA_TRY(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
-  // large n: two panels per pass -- factor panel k, update only panel k + 1's columns (thin
-  // SYRK), factor panel k + 1, then one trailing SYRK with both panels (K = 128): the trailing
-  // matrix (beyond L2) is read and written once per 128 columns
-  auto panel = [&](int64_t k0) -> ganq_status_t {
-    potrf_diag_kernel<<<1, 256, kPotrfSmem, st>>>(A, n, k0, d_status);
+  auto panel = [&](int64_t k0, cudaStream_t ps) -> ganq_status_t {
+    potrf_diag_kernel<<<1, 256, kPotrfSmem, ps>>>(A, n, k0, d_status);
     GANQ_LAUNCH_CHECK("potrf_diag_kernel");
     const int64_t rest = n - k0 - NB;
     if (rest > 0) {
-      trsm_panel_kernel<<<(unsigned)((rest + TR - 1) / TR), TR, kTrsmSmem, st>>>(A, n, k0);
+      trsm_panel_kernel<<<(unsigned)((rest + TR - 1) / TR), TR, kTrsmSmem, ps>>>(A, n, k0);
       GANQ_LAUNCH_CHECK("trsm_panel_kernel");
     }
     return GANQ_OK;
@@ -314,21 +334,42 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t 
     return GANQ_OK;
   };
   if (n < 6144) {
-    // the trailing matrix (<= 300 MB) largely stays in L2: one panel per pass (fewer launches)
+    // One panel per pass with look-ahead: the trailing update of panel k is split into a thin
+    // update of panel k+1's columns and the bulk (columns beyond); panel k+1's diagonal factor
+    // and TRSM run on a side stream while the bulk update of panel k runs on `st`.
+    //   side:  potrf(k+1), trsm(k+1)    after thin(k)          (event th)
+    //   st:    thin(k+1)                after trsm(k+1)        (event tr)
+    // thin(k) follows bulk(k-1) on st, so panel k+1 has every earlier update when it starts.
+    LookAhead& la = look_ahead();
+    GANQ_CUDA_TRY(cudaEventRecord(la.th, st));
+    GANQ_CUDA_TRY(cudaStreamWaitEvent(la.side, la.th, 0));
+    ganq_status_t s;
+    if ((s = panel(0, la.side))) return s;
+    GANQ_CUDA_TRY(cudaEventRecord(la.tr, la.side));
     for (int64_t k0 = 0; k0 < n; k0 += NB) {
-      ganq_status_t s;
-      if ((s = panel(k0))) return s;
-      if (k0 + NB >= n) break;
-      if ((s = syrk(k0, NB, k0 + NB, n))) return s;
+      const int64_t k1 = k0 + NB;
+      if (k1 >= n) break;
+      GANQ_CUDA_TRY(cudaStreamWaitEvent(st, la.tr, 0));  // trsm(k) done
+      if ((s = syrk(k0, NB, k1, min(k1 + NB, n)))) return s;  // thin(k): panel k+1's columns
+      GANQ_CUDA_TRY(cudaEventRecord(la.th, st));
+      GANQ_CUDA_TRY(cudaStreamWaitEvent(la.side, la.th, 0));
+      if ((s = panel(k1, la.side))) return s;                // overlaps bulk(k) below
+      GANQ_CUDA_TRY(cudaEventRecord(la.tr, la.side));
+      if (k1 + NB < n)
+        if ((s = syrk(k0, NB, k1 + NB, n))) return s;        // bulk(k)
     }
+    GANQ_CUDA_TRY(cudaStreamWaitEvent(st, la.tr, 0));      // the last panel is factored
   } else {
+    // large n: two panels per pass -- factor panel k, update only panel k + 1's columns (thin
+    // SYRK), factor panel k + 1, then one trailing SYRK with both panels (K = 128): the trailing
+    // matrix (beyond L2) is read and written once per 128 columns
     for (int64_t k0 = 0; k0 < n; k0 += 2 * NB) {
       ganq_status_t s;
-      if ((s = panel(k0))) return s;
+      if ((s = panel(k0, st))) return s;
       const int64_t k1 = k0 + NB;
       if (k1 >= n) break;
       if ((s = syrk(k0, NB, k1, min(k1 + NB, n)))) return s;  // panel k+1's columns only
-      if ((s = panel(k1))) return s;
+      if ((s = panel(k1, st))) return s;
       const int64_t base = k1 + NB;
       if (base >= n) break;
       if ((s = syrk(k0, 2 * NB, base, n))) return s;          // trailing block, both panels
