@@ -362,7 +362,8 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t 
   } else {
     // large n: two panels per pass -- factor panel k, update only panel k + 1's columns (thin
     // SYRK), factor panel k + 1, then one trailing SYRK with both panels (K = 128): the trailing
-    // matrix (beyond L2) is read and written once per 128 columns
+    // matrix (beyond L2) is read and written once per 128 columns.  (Look-ahead on the side
+    // stream was measured slower here: the HBM-bound bulk update loses SMs to the panel kernels.)
     for (int64_t k0 = 0; k0 < n; k0 += 2 * NB) {
       ganq_status_t s;
       if ((s = panel(k0, st))) return s;
