@@ -93,17 +93,22 @@ __global__ void hdiag_kernel(const double* __restrict__ H, int64_t n, double* __
   if (j < n) hdiag[j] = H[j * n + j];
 }
 
-// One warp per row; lane l < NLEV holds row l of the (regularised) system.
+// 32 / NLEV rows per warp, each in a segment of NLEV lanes; lane l of a segment holds row l of
+// that row's (regularised) 2^N x 2^N system.  Shuffles stay inside the segment (width NLEV).
 template <int NLEV>
 __global__ void __launch_bounds__(256)
 tsolve_kernel(double* __restrict__ G, const double* __restrict__ Dv, const double* __restrict__ bvec,
               const int* __restrict__ cnt, int64_t m, int empty_rule, float* __restrict__ T,
               int* __restrict__ fallback) {
+  constexpr int RPW = 32 / NLEV;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
-  if (row >= m) return;
-  const int l = lane < NLEV ? lane : 0;
-  const bool used = cnt[row * NLEV + l] > 0;
+  const int seg = lane / NLEV, l = lane % NLEV;
+  const int64_t row = ((int64_t)blockIdx.x * 8 + warp) * RPW + seg;
+  const bool live = row < m;
+  const int64_t rw = live ? row : 0;  // (dead segments compute on row 0 and write nothing)
+  const bool used = live && cnt[rw * NLEV + l] > 0;
+  auto sh = [](double v, int c) { return __shfl_sync(0xffffffffu, v, c, NLEV); };
+  auto shi = [](int v, int c) { return __shfl_sync(0xffffffffu, v, c, NLEV); };
   double g[NLEV];
   double maxdiag = 0.0;
   // assemble G = C + C^T + D; C (strict lower sums j > k) arrives as GANQ_TGRAM_SPLIT
@@ -113,75 +118,76 @@ tsolve_kernel(double* __restrict__ G, const double* __restrict__ Dv, const doubl
   for (int c = 0; c < NLEV; ++c) {
     double clc = 0.0, ccl = 0.0;
     for (int p = 0; p < kTgramSplit; ++p) {
-      clc += G[p * pstride + (row * NLEV + l) * NLEV + c];
-      ccl += G[p * pstride + (row * NLEV + c) * NLEV + l];
+      clc += G[p * pstride + (rw * NLEV + l) * NLEV + c];
+      ccl += G[p * pstride + (rw * NLEV + c) * NLEV + l];
     }
-    g[c] = clc + ccl + (c == l ? Dv[row * NLEV + l] : 0.0);
+    g[c] = clc + ccl + (c == l ? Dv[rw * NLEV + l] : 0.0);
   }
   __syncwarp();
-  if (lane < NLEV) {
+  if (live) {
 #pragma unroll
-    for (int c = 0; c < NLEV; ++c) G[(row * NLEV + l) * NLEV + c] = g[c];  // full G for the pinv path
+    for (int c = 0; c < NLEV; ++c) G[(rw * NLEV + l) * NLEV + c] = g[c];  // full G for the pinv path
   }
 #pragma unroll
   for (int c = 0; c < NLEV; ++c) {
-    const bool usedc = __shfl_sync(0xffffffffu, used ? 1 : 0, c) != 0;
+    const bool usedc = shi(used ? 1 : 0, c) != 0;
     g[c] = (used && usedc) ? g[c] : ((c == l && !used) ? 1.0 : 0.0);
   }
 #pragma unroll
   for (int c = 0; c < NLEV; ++c) {
-    const double d = __shfl_sync(0xffffffffu, g[c], c);
-    const bool uc = __shfl_sync(0xffffffffu, used ? 1 : 0, c) != 0;
+    const double d = sh(g[c], c);
+    const bool uc = shi(used ? 1 : 0, c) != 0;
     if (uc && d > maxdiag) maxdiag = d;
   }
-  double x = used ? bvec[row * NLEV + l] : 0.0;
+  double x = used ? bvec[rw * NLEV + l] : 0.0;
   const double tol = (double)NLEV * 2.220446049250313e-16 * maxdiag;
   bool ok = true;
   // Cholesky G = L L^T (lane l keeps row l of L in g[0..l])
 #pragma unroll
   for (int c = 0; c < NLEV; ++c) {
-    const double piv = __shfl_sync(0xffffffffu, g[c], c);
+    const double piv = sh(g[c], c);
     if (!(piv > tol)) ok = false;
     const double lcc = sqrt(piv > 0.0 ? piv : 1.0);
-    double lic = (lane > c) ? g[c] / lcc : (lane == c ? lcc : 0.0);
-    if (lane < NLEV) g[c] = lic;
+    const double lic = (l > c) ? g[c] / lcc : (l == c ? lcc : 0.0);
+    g[c] = lic;
 #pragma unroll
     for (int q = c + 1; q < NLEV; ++q) {
-      const double lqc = __shfl_sync(0xffffffffu, lic, q);
-      if (lane > c && q <= lane) g[q] -= lic * lqc;
+      const double lqc = sh(lic, q);
+      if (l > c && q <= l) g[q] -= lic * lqc;
     }
   }
   // forward: L y = b
 #pragma unroll
   for (int c = 0; c < NLEV; ++c) {
-    const double lcc = __shfl_sync(0xffffffffu, g[c], c);
-    const double yc = __shfl_sync(0xffffffffu, x, c) / lcc;
-    if (lane == c) x = yc;
-    else if (lane > c) x -= g[c] * yc;
+    const double lcc = sh(g[c], c);
+    const double yc = sh(x, c) / lcc;
+    if (l == c) x = yc;
+    else if (l > c) x -= g[c] * yc;
   }
   // backward: L^T t = y  (L^T row c = column c of L: lane q holds L[q][c] in g[c])
 #pragma unroll
   for (int c = NLEV - 1; c >= 0; --c) {
-    const double lcc = __shfl_sync(0xffffffffu, g[c], c);
-    const double tc = __shfl_sync(0xffffffffu, x, c) / lcc;
-    if (lane == c) x = tc;
+    const double lcc = sh(g[c], c);
+    const double tc = sh(x, c) / lcc;
+    if (l == c) x = tc;
     // x_r -= L[c][r] * t_c for r < c : lane c holds L[c][r] = g[r]; broadcast per r
 #pragma unroll
     for (int r = 0; r < c; ++r) {
-      const double lcr = __shfl_sync(0xffffffffu, g[r], c);
-      if (lane == r) x -= lcr * tc;
+      const double lcr = sh(g[r], c);
+      if (l == r) x -= lcr * tc;
     }
   }
-  ok = __all_sync(0xffffffffu, ok);
-  if (!ok) {
-    if (lane == 0) fallback[row] = 1;
+  // the segment's rows are all usable, else its row takes the pseudo-inverse path
+  const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+  const unsigned segmask = (NLEV == 32 ? 0xffffffffu : ((1u << NLEV) - 1u)) << (seg * NLEV);
+  if (!live) return;
+  if (bad & segmask) {
+    if (l == 0) fallback[row] = 1;
     return;
   }
-  if (lane < NLEV) {
-    float out = (float)x;
-    if (!used) out = (empty_rule == 1) ? T[row * NLEV + lane] : 0.0f;
-    T[row * NLEV + lane] = out;
-  }
+  float out = (float)x;
+  if (!used) out = (empty_rule == 1) ? T[row * NLEV + l] : 0.0f;
+  T[row * NLEV + l] = out;
 }
 
 // Rare path: Moore-Penrose by cyclic Jacobi (one thread per flagged row, fp64).
@@ -277,7 +283,8 @@ ganq_status_t launch_tsolve_t(const double* hdiag, const float* WH, const uint8_
   trhs_kernel<NLEV><<<(unsigned)((m + TRHS_WARPS - 1) / TRHS_WARPS), 32 * TRHS_WARPS, 0, st>>>(hdiag, WH, Q, m, n,
                                                                                                Dv, b, cnt);
   GANQ_LAUNCH_CHECK("trhs_kernel");
-  tsolve_kernel<NLEV><<<(unsigned)((m + 7) / 8), 256, 0, st>>>(G, Dv, b, cnt, m, empty_rule, T, fb);
+  tsolve_kernel<NLEV><<<(unsigned)((m + 8 * (32 / NLEV) - 1) / (8 * (32 / NLEV))), 256, 0, st>>>(G, Dv, b, cnt, m,
+                                                                                           empty_rule, T, fb);
   GANQ_LAUNCH_CHECK("tsolve_kernel");
   tsolve_pinv_kernel<NLEV><<<(unsigned)((m + 127) / 128), 128, 0, st>>>(G, b, cnt, m, empty_rule, T,
                                                                          fb);
