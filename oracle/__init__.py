@@ -71,6 +71,8 @@ def _load():
         lib.or_outlier_split.restype = None
         lib.or_sparse_matmul.argtypes = [P, P, P, I64, I64, P, I64, P]
         lib.or_sparse_matmul.restype = None
+        lib.or_kmeans_codebook.argtypes = [P, I64, I64, ctypes.c_int, ctypes.c_int, P]
+        lib.or_kmeans_codebook.restype = None
         lib.or_init_codebook.argtypes = [P, I64, I64, ctypes.c_int, P]
         lib.or_init_codebook.restype = None
         lib.or_sstep.argtypes = [P, P, P, I64, I64, ctypes.c_int, P, P]
@@ -304,3 +306,14 @@ def sparse_matmul(off, col, val, m: int, n: int, X) -> np.ndarray:
     Y = np.zeros((p, m), np.float64)
     lib.or_sparse_matmul(off.ctypes.data, col.ctypes.data, val.ctypes.data, m, n, X.ctypes.data, p, Y.ctypes.data)
     return Y
+
+
+# --------------------------------------------------------------------------- NEXT-4
+def kmeans_codebook(W, nbits: int, iters: int) -> np.ndarray:
+    """Per-row 1-D Lloyd from the min-max grid (reading R-24): fp32 m x 2^N."""
+    lib = _load()
+    W = np.ascontiguousarray(W, dtype=np.float32)
+    m, n = W.shape
+    T = np.zeros((m, 1 << nbits), np.float32)
+    lib.or_kmeans_codebook(W.ctypes.data, m, n, 1 << nbits, iters, T.ctypes.data)
+    return T

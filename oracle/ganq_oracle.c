@@ -572,3 +572,35 @@ void or_sparse_matmul(const int64_t *off, const int32_t *col, const float *val, 
             Y[t * m + i] = acc;
         }
 }
+
+/* ========================================================================= */
+/* NEXT-4: k-means initial codebook (per-row 1-D Lloyd), reading R-24.        */
+/* ========================================================================= */
+/* T0 = iters Lloyd iterations per row from the min-max grid of or_init_codebook [R-6]:
+ * assign w_j to argmin_s |w_j - t_s| (fp64 distance of fp32 values, exact; first index on
+ * ties [R-7]); t_s <- mean of its weights (fp64), empty levels keep their value; t_s rounded to
+ * fp32 after each iteration (T0 is an fp32 input of Algorithm 1). */
+void or_kmeans_codebook(const float *W, int64_t m, int64_t n, int nlev, int iters, float *T0) {
+    or_init_codebook(W, m, n, nlev, T0);
+#pragma omp parallel
+    {
+        double *sum = (double *)malloc(sizeof(double) * (size_t)nlev);
+        int64_t *cnt = (int64_t *)malloc(sizeof(int64_t) * (size_t)nlev);
+        double *t = (double *)malloc(sizeof(double) * (size_t)nlev);
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < m; ++i) {
+            for (int it = 0; it < iters; ++it) {
+                for (int s = 0; s < nlev; ++s) { sum[s] = 0.0; cnt[s] = 0; t[s] = (double)T0[i * nlev + s]; }
+                for (int64_t j = 0; j < n; ++j) {
+                    const double w = (double)W[i * n + j];
+                    const int q = argmin_level(w, t, nlev);
+                    sum[q] += w;
+                    cnt[q] += 1;
+                }
+                for (int s = 0; s < nlev; ++s)
+                    if (cnt[s] > 0) T0[i * nlev + s] = (float)(sum[s] / (double)cnt[s]);
+            }
+        }
+        free(sum); free(cnt); free(t);
+    }
+}
