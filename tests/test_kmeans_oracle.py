@@ -89,3 +89,41 @@ def test_kmeans_constant_and_empty_levels(oracle):
     g = oracle.init_codebook(W, 3)[1]
     assert T[1, 0] == -1.0 and T[1, 7] == 1.0
     np.testing.assert_array_equal(T[1, 1:7], g[1:7])
+
+
+def _dp_optimal_sse(w, k):
+    """Exact 1-D k-clustering by dynamic programming over the sorted row (clusters are contiguous)."""
+    x = np.sort(np.asarray(w, np.float64))
+    n = len(x)
+    c1 = np.concatenate([[0.0], np.cumsum(x)])
+    c2 = np.concatenate([[0.0], np.cumsum(x * x)])
+
+    def sse(a, b):  # x[a:b]
+        s = c1[b] - c1[a]
+        return max(c2[b] - c2[a] - s * s / (b - a), 0.0)
+
+    D = np.full((k + 1, n + 1), np.inf)
+    D[0, 0] = 0.0
+    for c in range(1, k + 1):
+        for b in range(c, n + 1):
+            D[c, b] = min(D[c - 1, a] + sse(a, b) for a in range(c - 1, b))
+    return D[k, n]
+
+
+def test_kmeans_spec_examples(oracle):
+    T = oracle.kmeans_codebook(np.array([[0, 3, 3, 3]], np.float32), 1, 25)  # SPEC S:207
+    np.testing.assert_array_equal(np.sort(T[0]), [0.0, 3.0])
+    T = oracle.kmeans_codebook(np.array([[0, 0, 10, 10]], np.float32), 1, 25)  # SPEC S:304
+    np.testing.assert_array_equal(np.sort(T[0]), [0.0, 10.0])
+
+
+def test_kmeans_near_dp_optimum(oracle):
+    """SPEC S:208's derived check: 25 Lloyd iterations within 5 % of the DP-optimal SSE (median)."""
+    rng = np.random.default_rng(6)
+    ratios = []
+    for seed in range(60):
+        w = rng.normal(size=48).astype(np.float32)
+        T = oracle.kmeans_codebook(w[None, :], 2, 25)
+        ratios.append(_distortion(w[None, :], T)[0] / _dp_optimal_sse(w, 4))
+    assert min(ratios) >= 1 - 1e-6
+    assert np.median(ratios) <= 1.05
