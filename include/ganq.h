@@ -216,6 +216,19 @@ ganq_status_t ganq_outlier_csr(const float* W, int64_t m, int64_t n, const float
 ganq_status_t ganq_sparse_gemm_add(const int64_t* row_offsets, const int32_t* col_idx, const float* values,
                                    int64_t m, int64_t n, const uint16_t* X, int64_t p, float* Y, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-4: k-means T^0
+ * ganq_kmeans_codebook: T (DEVICE fp32 m x 2^N, written) = per-row 1-D Lloyd k-means of W (DEVICE
+ * fp32 m x n row-major) started from the fp32 min-max grid (R-6): `iters` iterations of
+ * {nearest level, first index on ties; each non-empty level <- fp64 mean of its weights, rounded
+ * to fp32; empty levels keep their value} (reading R-24 -- Algorithm 1 takes T^0 as an
+ * input; k-means is the Euclidean-distance baseline of
+ * the related work).  iters = 0
+ * gives the grid itself.  Pass the result as ganq_quantize_opts_t.T0.  n_bits in [1, 4] (else
+ * GANQ_ERR_UNSUPPORTED), iters >= 0.  Async on `stream`.
+ */
+ganq_status_t ganq_kmeans_codebook(const float* W, int64_t m, int64_t n, int n_bits, int iters, float* T,
+                                   void* stream);
+
 const char* ganq_version(void);
 
 #ifdef __cplusplus

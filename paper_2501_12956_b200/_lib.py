@@ -46,6 +46,7 @@ SIG = {
     "ganq_outlier_split": (I32, [P, I64, I64, ctypes.c_double, P, P, P, P, P, P]),
     "ganq_outlier_csr": (I32, [P, I64, I64, P, P, P, P, P, P]),
     "ganq_sparse_gemm_add": (I32, [P, P, P, I64, I64, P, I64, P, P]),
+    "ganq_kmeans_codebook": (I32, [P, I64, I64, I32, I32, P, P]),
 }
 
 

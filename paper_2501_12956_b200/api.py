@@ -94,11 +94,17 @@ def _opts(precond, lam, tau, T0, empty_level_rule, trace_buf):
 def quantize_layer(W: torch.Tensor, H: torch.Tensor, n_bits: int, iters: int = 10, *,
                    precond: str = "adaptive", lam: float = 0.0, tau: float = 1e-7,
                    T0: torch.Tensor | None = None, empty_level_rule: int = 0, trace: bool = False,
-                   Q: torch.Tensor | None = None, T: torch.Tensor | None = None, stream=None):
+                   Q: torch.Tensor | None = None, T: torch.Tensor | None = None, stream=None,
+                   init: str = "grid", kmeans_iters: int = 25):
     """Algorithm 1 given H: returns (Q uint8 m x n, T fp32 m x 2^N[, obj_trace]).
 
     precond: "adaptive" (App. A, default), "fixed_lambda" (H + lam I, Remark 1), "none", or
-    "auto" (none, falling back to adaptive on a non-positive pivot)."""
+    "auto" (none, falling back to adaptive on a non-positive pivot).
+    init (when T0 is None): "grid" (fp32 min-max grid, R-6) or "kmeans" (kmeans_codebook, R-24)."""
+    if T0 is None and init == "kmeans":
+        T0 = kmeans_codebook(W, n_bits, kmeans_iters, stream=stream)
+    elif init not in ("grid", "kmeans"):
+        raise ValueError(f"init must be 'grid' or 'kmeans', got {init!r}")
     if precond == "auto":
         # NEXT-4 "on failure only": no preconditioning unless the factor hits a non-positive
         # pivot, then the adaptive shift of App. A (P:460-467)
@@ -194,6 +200,19 @@ def pack_codes(Q, n_bits: int, stream=None, check: bool = True):
     P = torch.empty((m, int(lib.ganq_packed_row_bytes(n, int(n_bits)))), dtype=torch.uint8, device=Q.device)
     _lib.check(lib.ganq_pack_codes(_ptr(Q), m, n, int(n_bits), _ptr(P), _stream(stream)))
     return P
+
+
+def kmeans_codebook(W, n_bits: int, iters: int = 25, T=None, stream=None):
+    """T^0 = per-row 1-D Lloyd k-means of W from the min-max grid (NEXT-4, reading R-24):
+    fp32 m x 2^N on W's device."""
+    _need(W, torch.float32, 2, "W")
+    m, n = W.shape
+    if T is None:
+        T = torch.empty((m, 1 << int(n_bits)), dtype=torch.float32, device=W.device)
+    _need(T, torch.float32, 2, "T")
+    _lib.check(_lib.load().ganq_kmeans_codebook(_ptr(W), m, n, int(n_bits), int(iters), _ptr(T),
+                                                _stream(stream)))
+    return T
 
 
 def codebook_f16(T, stream=None):

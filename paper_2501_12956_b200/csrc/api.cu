@@ -345,6 +345,21 @@ ganq_status_t ganq_sparse_gemm_add(const int64_t* row_offsets, const int32_t* co
   return launch_sparse_gemm_add(row_offsets, col_idx, values, m, n, X, p, Y, (cudaStream_t)stream);
 }
 
+ganq_status_t ganq_kmeans_codebook(const float* W, int64_t m, int64_t n, int n_bits, int iters, float* T,
+                                   void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (m < 1 || n < 1 || n_bits < 1 || n_bits > 8 || iters < 0 || !W || !T) {
+    set_error(GANQ_ERR_INVALID_ARG, "kmeans_codebook: need m, n >= 1, n_bits in [1, 8], iters >= 0, non-null buffers");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  if (n_bits > 4) {
+    set_error(GANQ_ERR_UNSUPPORTED, "kmeans_codebook: n_bits = %d, this build supports N <= 4", n_bits);
+    return GANQ_ERR_UNSUPPORTED;
+  }
+  return launch_kmeans_codebook(W, m, n, 1 << n_bits, iters, T, (cudaStream_t)stream);
+}
+
 const char* ganq_version(void) { return "ganq-b200 0.1 (sm_100a)"; }
 
 ganq_status_t ganq_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate,

@@ -41,6 +41,8 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t 
 ganq_status_t launch_derive_operands(const double* L, const double* H, int64_t n, float* Lhat,
                                      float* H32, cudaStream_t st);
 // tstep.cu
+ganq_status_t launch_kmeans_codebook(const float* W, int64_t m, int64_t n, int nlev, int iters, float* T,
+                                     cudaStream_t st);
 ganq_status_t launch_init_codebook(const float* W, int64_t m, int64_t n, int nlev, float* T,
                                    cudaStream_t st);
 // the T-update after the normal matrices (launch_tgram_tc): right-hand sides and the solves

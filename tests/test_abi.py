@@ -84,6 +84,9 @@ def test_argument_errors_without_gpu(lib):
     assert st == _lib.ERR_WORKSPACE
     st = lib.ganq_hessian(P, 0, 8, P, 0, None)
     assert st == _lib.ERR_INVALID_ARG
+    assert lib.ganq_kmeans_codebook(P, 4, 8, 2, -1, P, None) == _lib.ERR_INVALID_ARG
+    assert lib.ganq_kmeans_codebook(P, 4, 8, 5, 3, P, None) == _lib.ERR_UNSUPPORTED
+    assert lib.ganq_kmeans_codebook(None, 4, 8, 2, 3, P, None) == _lib.ERR_INVALID_ARG
 
 
 def test_binding_rejects_cpu_tensors():
@@ -100,6 +103,8 @@ def test_lut_binding_rejects_host_tensors():
     import paper_2501_12956_b200 as g
     with pytest.raises(ValueError, match="CUDA"):
         g.pack_codes(torch.zeros((2, 8), dtype=torch.uint8), 4)
+    with pytest.raises(ValueError, match="CUDA"):
+        g.kmeans_codebook(torch.zeros((2, 8)), 2)
 
 
 def test_packed_row_bytes(lib):
