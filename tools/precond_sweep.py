@@ -2,7 +2,8 @@
 layer: the objective ||WX - W~X||_F^2 after K = 10 iterations (instead of WikiText-2 perplexity,
 which needs a model and data) for H + lambda p I with lambda in {0.5, 1, 10, 40, 100} (Table 7's
 values for the normalised Hessian XX^T / p, reading R-23), the adaptive method of Eqs. 23-24,
-no preconditioning, and "auto" (none unless the factor fails); plus both empty-level rules.
+no preconditioning, and "auto" (none unless the factor fails); plus both empty-level rules and
+the k-means initial codebook (R-24).
 
     python tools/precond_sweep.py [--rows 4096] > profiles/r01_precond_sweep.md
 """
@@ -45,6 +46,9 @@ run("adaptive (Eqs. 23-24)", precond="adaptive")
 run("none", precond="none")
 run("auto (none unless not PD)", precond="auto")
 run("adaptive, keep-previous empty levels", precond="adaptive", empty_level_rule=1)
+run("adaptive, k-means T0 (25 Lloyd iterations, R-24)", precond="adaptive", init="kmeans")
+run("none, k-means T0 (25 Lloyd iterations, R-24)", precond="none", init="kmeans")
+run("fixed lambda = 100 (x p), k-means T0", precond="fixed_lambda", lam=100.0 * p, init="kmeans")
 best = min(r["objective"] for r in rows)
 print(f"# Preconditioning sweep, {args.config}: W {m} x {n}, {nbits}-bit, p = {p}, K = {K} (synthetic, seeds 1000/2000)\n")
 print("Structure of Table 7 (P:470-491); objective ||WX - W~X||_F^2 after K iterations (lower is better).\n")
