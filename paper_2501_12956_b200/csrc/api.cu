@@ -118,7 +118,7 @@ Layout make_layout(int64_t m, int64_t n, int nlev) {
   L.Xlo = take((size_t)m * kp * sizeof(float));
   L.Hhi = take((size_t)n * kp * sizeof(float));  // tf32 split of H32
   L.Hlo = take((size_t)n * kp * sizeof(float));
-  L.status = take(sizeof(int));
+  L.status = take(2 * sizeof(int));  // [0] first non-positive pivot, [1] panel-kernel ticket
   L.mean = take(sizeof(double));
   L.per_row = take((size_t)m * sizeof(double));
   L.total_d = take(sizeof(double));
@@ -185,9 +185,10 @@ ganq_status_t factor(const double* H, int64_t n, const ganq_opts_t& o, void* ws,
     if (s) return s;
   }
   GANQ_CUDA_TRY(cudaMemsetAsync(status, 0x7f, sizeof(int), st));
+  GANQ_CUDA_TRY(cudaMemsetAsync(status + 1, 0, sizeof(int), st));
   {
     GANQ_STAGE(ST_CHOLESKY);
-    if ((s = launch_cholesky(A, n, status, st))) return s;
+    if ((s = launch_cholesky(A, n, status, status + 1, st))) return s;
   }
   int h_status = 0;
   GANQ_CUDA_TRY(cudaMemcpyAsync(&h_status, status, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -3,9 +3,9 @@
 // fp32 operands the S- and T-updates read (reading R-10).
 //
 // Factorisation: right-looking blocked Cholesky with NB = 64, in place on the lower
-// triangle of A (fp64).  Per block column k: (1) one CTA factors the 64 x 64 diagonal
-// block in shared memory, (2) TRSM of the panel below it (thread per row, forward
-// substitution from shared memory), (3) trailing SYRK update of the lower tiles (128 x 128
+// triangle of A (fp64).  Per block column k: (1) one launch factors the 64 x 64 diagonal
+// block and solves the panel below it (every CTA eliminates the diagonal block plus 64 panel
+// rows in registers), (2) trailing SYRK update of the lower tiles (128 x 128
 // tiles, 8 x 8 fp64 register blocking), applied once per two panels (K = 128).  Each tile has
 // one owner per step, so the result is deterministic (bitwise identical on every rank).
 // A non-positive pivot records its global index (atomicMin) in *d_status.
@@ -75,116 +75,113 @@ __global__ void precondition_kernel(const double* __restrict__ H, int64_t n, int
   }
 }
 
-// ---------------------------------------------------------------- diagonal block
-// One CTA of 256 threads = 16 x 16; thread (tx, ty) owns the 4 x 4 elements
-// (ty + 16 a, tx + 16 b) of the 64 x 64 block.  Unscaled elimination with one barrier per
-// column: step c subtracts a_rc a_qc / d_c from the trailing elements (d_c = a_cc, the pivot),
-// which equals L_rc L_qc of the standard algorithm; afterwards L_rc = a_rc / sqrt(d_c).
-__global__ void __launch_bounds__(256) potrf_diag_kernel(double* __restrict__ A, int64_t n, int64_t k0,
-                                                         int* __restrict__ status) {
-  extern __shared__ double potrf_smem[];
-  double* s = potrf_smem;               // [64][LDS] the block
-  double* dpiv = potrf_smem + NB * LDS; // [64] pivots
+// ---------------------------------------------------------------- panel factor (POTRF + TRSM)
+// Block column k0 (kb <= 64 columns) of the right-looking factorisation, restricted to its own
+// columns: every CTA holds the 64 x 64 diagonal block plus PR rows of the panel below it and
+// runs the unscaled elimination on those 128 rows -- step c subtracts a_rc a_qc / d_c from the
+// elements right of column c (d_c = a_cc, the pivot), which for the panel rows is exactly the
+// forward substitution x L_kk^T = A_panel and for the diagonal block the Cholesky of L_kk;
+// afterwards L_rc = a_rc / sqrt(d_c).  The diagonal block is factored redundantly by every
+// CTA (same instructions, same result), so POTRF and TRSM are one launch whose dependent chain
+// is 64 column steps of {one barrier, one broadcast read of column c, 32 FMAs per thread}.
+// Thread (tx, ty) keeps its 8 x 4 elements (ty + 16 a, tx + 16 b) in registers; the owners of
+// column c publish it to shared memory (double-buffered, one barrier per step).  The CTA that
+// finishes last writes the diagonal block (every other CTA has read its input by then -- CTAs
+// of a large grid, or ones delayed behind another stream's kernel, start late); a non-positive
+// pivot records its global index in *status.
+constexpr int PR = 64;          // panel rows per CTA
+constexpr int PROWS = NB + PR;  // rows held per CTA
+constexpr int PF_THREADS = 256; // thread (tx, ty): rows ty + 16 a (a < 8), columns tx + 16 b (b < 4)
+// 1 / d to ~1 ulp: hardware estimate + two Newton steps (no slow-path branch on the chain)
+__device__ __forceinline__ double rcp_nr(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = r * fma(-d, r, 2.0);
+  return r * fma(-d, r, 2.0);
+}
+__global__ void __launch_bounds__(PF_THREADS) panel_factor_kernel(double* __restrict__ A, int64_t n, int64_t k0,
+                                                                  int* __restrict__ status, int* __restrict__ ticket) {
+  __shared__ double col[2 * PROWS];  // column c of the 128 rows, double-buffered
+  __shared__ double dpiv[NB];
+  __shared__ int last;
   const int kb = (int)min((int64_t)NB, n - k0);
+  const int64_t p0 = k0 + kb + (int64_t)blockIdx.x * PR;  // first panel row of this CTA
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  // element (ty + 16 a, tx + 16 b); a < 4: the diagonal block, a >= 4: panel rows
+  double v[8][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int r = ty + 16 * a, c = tx + 16 * b;
-      s[r * LDS + c] = (r < kb && c <= r) ? A[(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
-    }
-  __syncthreads();
-  for (int c = 0; c < NB; ++c) {
-    double d = s[c * LDS + c];
-    if (!(d > 0.0)) {  // not positive definite (or NaN)
-      if (threadIdx.x == 0 && c < kb) atomicMin(status, (int)(k0 + c));
-      d = 1.0;
-    }
-    if (threadIdx.x == 0) dpiv[c] = d;
-    const double id = 1.0 / d;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int r = ty + 16 * a;
-      if (r <= c) continue;
-      const double arc = s[r * LDS + c] * id;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int q = tx + 16 * b;
-        if (q > c && q <= r) s[r * LDS + q] -= arc * s[q * LDS + c];
+      const int r = ty + 16 * a, q = tx + 16 * b;
+      if (a < NB / 16) {
+        v[a][b] = (r < kb && q <= r) ? A[(k0 + r) * n + k0 + q] : (r == q ? 1.0 : 0.0);
+      } else {
+        const int64_t i = p0 + (r - NB);
+        v[a][b] = (i < n && q < kb) ? A[i * n + k0 + q] : 0.0;
       }
     }
-    __syncthreads();
-  }
-  // L_rc = a_rc / sqrt(d_c), L_cc = sqrt(d_c)
+  // Column c = 16 bc + cl: its owners are the threads with tx == cl (register slot b = bc, a
+  // compile-time index).  Step c updates (r, q) with r > c and q > c: column blocks b < bc are
+  // final and skipped, block bc is masked by q > c, diagonal-block rows by r > c.
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int bc = 0; bc < 4; ++bc) {
+#pragma unroll 1
+    for (int cl = 0; cl < 16; ++cl) {
+      const int c = 16 * bc + cl;
+      const int buf = (c & 1) * PROWS;
+      if (tx == cl) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a) col[buf + ty + 16 * a] = v[a][bc];
+      }
+      __syncthreads();
+      double d = col[buf + c];
+      double cr[8], cq[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) cr[a] = (a >= NB / 16 || ty + 16 * a > c) ? col[buf + ty + 16 * a] : 0.0;
+#pragma unroll
+      for (int b = bc; b < 4; ++b) cq[b] = (b > bc || tx > cl) ? col[buf + tx + 16 * b] : 0.0;
+      if (!(d > 0.0)) {  // not positive definite (or NaN)
+        if (threadIdx.x == 0 && blockIdx.x == 0 && c < kb) atomicMin(status, (int)(k0 + c));
+        d = 1.0;
+      }
+      if (threadIdx.x == 0) dpiv[c] = d;
+      const double id = rcp_nr(d);
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const double t = cr[a] * id;
+#pragma unroll
+        for (int b = bc; b < 4; ++b) v[a][b] = fma(-t, cq[b], v[a][b]);
+      }
+    }
+  }
+  __syncthreads();
+  // L_rq = a_rq / sqrt(d_q), L_qq = sqrt(d_q)
+  double sd[4], isd[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    sd[b] = sqrt(dpiv[tx + 16 * b]);
+    isd[b] = 1.0 / sd[b];
+  }
+#pragma unroll
+  for (int a = NB / 16; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int r = ty + 16 * a, c = tx + 16 * b;
-      const double sd = sqrt(dpiv[c]);
-      if (c < r) s[r * LDS + c] /= sd;
-      else if (c == r) s[r * LDS + c] = sd;
+      const int r = ty + 16 * a, q = tx + 16 * b;
+      const int64_t i = p0 + (r - NB);
+      if (i < n && q < kb) A[i * n + k0 + q] = v[a][b] * isd[b];
     }
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1) == (int)gridDim.x - 1);
   __syncthreads();
+  if (!last) return;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < NB / 16; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int r = ty + 16 * a, c = tx + 16 * b;
-      if (r < kb && c <= r) A[(k0 + r) * n + k0 + c] = s[r * LDS + c];
+      const int r = ty + 16 * a, q = tx + 16 * b;
+      if (r < kb && q <= r) A[(k0 + r) * n + k0 + q] = (q == r) ? sd[b] : v[a][b] * isd[b];
     }
-}
-
-// ---------------------------------------------------------------- panel TRSM
-// For rows i >= k0 + kb:  x = L[i, k0:k0+kb] solves x L_kk^T = A[i, k0:k0+kb], i.e. forward
-// substitution x_c = (a_c - sum_{q<c} x_q L_cq) / L_cc.  One thread per row (x in registers,
-// four interleaved partial sums per column), 128 rows per CTA staged through shared memory
-// (coalesced cp.async), L_kk in shared memory (broadcast reads).
-constexpr int TR = 128;
-__global__ void __launch_bounds__(TR) trsm_panel_kernel(double* __restrict__ A, int64_t n, int64_t k0) {
-  extern __shared__ double trsm_smem[];
-  double* Pr = trsm_smem;             // [TR][LDS] the CTA's panel rows
-  double* Lk = trsm_smem + TR * LDS;  // [NB][LDS] L_kk
-  double* rd = Lk + NB * LDS;         // [NB] 1 / L_cc
-  const int kb = (int)min((int64_t)NB, n - k0);
-  const int64_t i0 = k0 + kb + (int64_t)blockIdx.x * TR;
-  for (int e = threadIdx.x; e < TR * NB; e += TR) {
-    const int r = e >> 6, c = e & 63;
-    if (i0 + r < n && c < kb) cp8(&Pr[r * LDS + c], &A[(i0 + r) * n + k0 + c]);
-    else Pr[r * LDS + c] = 0.0;
-  }
-  for (int e = threadIdx.x; e < NB * NB; e += TR) {
-    const int r = e >> 6, c = e & 63;
-    if (r < kb && c <= r) cp8(&Lk[r * LDS + c], &A[(k0 + r) * n + k0 + c]);
-    else Lk[r * LDS + c] = (r == c) ? 1.0 : 0.0;
-  }
-  cp_wait();
-  __syncthreads();
-  if (threadIdx.x < NB) rd[threadIdx.x] = 1.0 / Lk[threadIdx.x * LDS + threadIdx.x];
-  __syncthreads();
-  const int r = threadIdx.x;
-  double x[NB];
-#pragma unroll
-  for (int c = 0; c < NB; ++c) {
-    double p0 = Pr[r * LDS + c], p1 = 0.0, p2 = 0.0, p3 = 0.0;
-#pragma unroll
-    for (int q = 0; q + 3 < c; q += 4) {
-      p0 = fma(-x[q], Lk[c * LDS + q], p0);
-      p1 = fma(-x[q + 1], Lk[c * LDS + q + 1], p1);
-      p2 = fma(-x[q + 2], Lk[c * LDS + q + 2], p2);
-      p3 = fma(-x[q + 3], Lk[c * LDS + q + 3], p3);
-    }
-#pragma unroll
-    for (int q = c & ~3; q < c; ++q) p0 = fma(-x[q], Lk[c * LDS + q], p0);
-    x[c] = ((p0 + p1) + (p2 + p3)) * rd[c];
-  }
-  const int64_t i = i0 + r;
-  if (i < n) {
-#pragma unroll
-    for (int c = 0; c < NB; ++c)
-      if (c < kb) A[i * n + k0 + c] = x[c];
-  }
+  if (threadIdx.x == 0) *ticket = 0;  // ready for the next panel launch (stream-ordered)
 }
 
 // ---------------------------------------------------------------- trailing SYRK
@@ -309,22 +306,15 @@ LookAhead& look_ahead() {
   return la;
 }
 
-ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t st) {
+ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket, cudaStream_t st) {
   constexpr int kSyrkSmem = 2 * ST * LDS * sizeof(double);
-  constexpr int kTrsmSmem = ((TR + NB) * LDS + NB) * sizeof(double);
-  constexpr int kPotrfSmem = (NB * LDS + NB) * sizeof(double);
-  GANQ_CUDA_TRY(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPotrfSmem));
   GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
-  GANQ_CUDA_TRY(cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTrsmSmem));
   auto panel = [&](int64_t k0, cudaStream_t ps) -> ganq_status_t {
-    potrf_diag_kernel<<<1, 256, kPotrfSmem, ps>>>(A, n, k0, d_status);
-    GANQ_LAUNCH_CHECK("potrf_diag_kernel");
     const int64_t rest = n - k0 - NB;
-    if (rest > 0) {
-      trsm_panel_kernel<<<(unsigned)((rest + TR - 1) / TR), TR, kTrsmSmem, ps>>>(A, n, k0);
-      GANQ_LAUNCH_CHECK("trsm_panel_kernel");
-    }
+    const unsigned grid = rest > 0 ? (unsigned)((rest + PR - 1) / PR) : 1u;
+    panel_factor_kernel<<<grid, PF_THREADS, 0, ps>>>(A, n, k0, d_status, d_ticket);
+    GANQ_LAUNCH_CHECK("panel_factor_kernel");
     return GANQ_OK;
   };
   auto syrk = [&](int64_t k0, int kw, int64_t base, int64_t cend) -> ganq_status_t {

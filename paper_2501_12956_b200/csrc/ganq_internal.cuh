@@ -37,7 +37,8 @@ ganq_status_t launch_hessian(const uint16_t* X, int64_t p, int64_t n, double* H,
 // cholesky.cu
 ganq_status_t launch_precondition(const double* H, int64_t n, int policy, double lambda, double tau,
                                   double* A, double* delta, double* d_mean, cudaStream_t st);
-ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, cudaStream_t st);
+// d_ticket: a device int that is 0 on entry (the panel kernel's completion counter; left 0)
+ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket, cudaStream_t st);
 ganq_status_t launch_derive_operands(const double* L, const double* H, int64_t n, float* Lhat,
                                      float* H32, cudaStream_t st);
 // tstep.cu

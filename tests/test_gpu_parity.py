@@ -92,9 +92,12 @@ def test_hessian_token_shards_sum():
 
 # ----------------------------------------------------------------------------- P-2 factor
 
-@pytest.mark.parametrize("policy", ["adaptive", "fixed_lambda", "none"])
-def test_factor_parity(policy):
-    _, X = make_case(4, 256, 4000, seed=7)
+@pytest.mark.parametrize("policy,n", [("adaptive", 256), ("fixed_lambda", 256), ("none", 256),
+                                      ("adaptive", 296), ("none", 1000), ("adaptive", 64), ("none", 72)])
+def test_factor_parity(policy, n):
+    """n spans one to 16 panels, a ragged last panel (296 = 4 x 64 + 40) and panel rows that
+    end mid-CTA (n must be a multiple of 8 for the bf16 activations' TMA rows)."""
+    _, X = make_case(4, n, 4000, seed=7)
     H = gpu_H(X)
     lam = 0.01 * float(torch.diagonal(H).mean()) if policy == "fixed_lambda" else 0.0
     L, delta = g.factor(H, policy, lam=lam)
