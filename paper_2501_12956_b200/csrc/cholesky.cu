@@ -226,26 +226,16 @@ __global__ void __launch_bounds__(256) syrk_trailing_kernel(double* __restrict__
         for (int y = 0; y < 8; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
     }
   }
-  // read-modify-write in two batches of 32: all loads of a batch are issued before its stores
-  // (the compiler keeps loads and stores through one pointer in order, one round trip each)
+  // A -= acc as fire-and-forget fp64 reductions in L2 (RED.ADD.F64): no load round trip on the
+  // SM; every element has exactly one owner per launch and launches are stream-ordered, so the
+  // result equals a read-modify-write bit for bit
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    double old[4][8];
+  for (int x = 0; x < 8; ++x)
 #pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 8; ++y) {
-        const int64_t i = i0 + ty + 16 * (4 * h + x), j = j0 + tx + 16 * y;
-        old[x][y] = (i < n && j <= i && j < cend) ? A[i * n + j] : 0.0;
-      }
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 8; ++y) {
-        const int64_t i = i0 + ty + 16 * (4 * h + x), j = j0 + tx + 16 * y;
-        if (i < n && j <= i && j < cend) A[i * n + j] = old[x][y] - acc[4 * h + x][y];
-      }
-  }
+    for (int y = 0; y < 8; ++y) {
+      const int64_t i = i0 + ty + 16 * x, j = j0 + tx + 16 * y;
+      if (i < n && j <= i && j < cend) atomicAdd(&A[i * n + j], -acc[x][y]);
+    }
 }
 
 __global__ void zero_upper_kernel(double* __restrict__ A, int64_t n) {
