@@ -25,6 +25,9 @@ constexpr int LDS = NB + 1;  // padded fp64 row stride in shared memory
 __device__ __forceinline__ void cp8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ---------------------------------------------------------------- precondition
@@ -185,57 +188,140 @@ __global__ void __launch_bounds__(PF_THREADS) panel_factor_kernel(double* __rest
 }
 
 // ---------------------------------------------------------------- trailing SYRK
-// A[i, j] -= sum_c L[i, k0+c] L[j, k0+c] for the lower 128 x 128 tiles of the trailing matrix;
-// thread (tx, ty) owns the 8 x 8 elements (ty + 16 x, tx + 16 y) of its tile.
-constexpr int ST = 128;  // SYRK tile
 // A[i, j] -= sum_{c in [k0, k0 + kw)} L[i, c] L[j, c] for base <= j <= i < n, j < cend: the lower
-// 128 x 128 tiles of the trailing block, the kw <= 128 panel columns streamed through shared
-// memory in chunks of 64 (the accumulators stay in registers, one read-modify-write per tile).
-__global__ void __launch_bounds__(256) syrk_trailing_kernel(double* __restrict__ A, int64_t n, int64_t k0,
-                                                            int kw, int64_t base, int64_t cend) {
-  const int ti = blockIdx.y, tj = blockIdx.x;
-  if (tj > ti) return;
-  extern __shared__ double syrk_smem[];
-  double* Pi = syrk_smem;
-  double* Pj = syrk_smem + ST * LDS;
-  const int64_t i0 = base + (int64_t)ti * ST, j0 = base + (int64_t)tj * ST;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double acc[8][8] = {};
-  for (int kc = 0; kc < kw; kc += NB) {
-    const int kcw = min(NB, kw - kc);
-    if (kc > 0) __syncthreads();  // the previous chunk has been consumed
-    for (int e = threadIdx.x; e < ST * NB; e += 256) {
-      const int r = e >> 6, c = e & 63;
-      if (i0 + r < n && c < kcw) cp8(&Pi[r * LDS + c], &A[(i0 + r) * n + k0 + kc + c]);
-      else Pi[r * LDS + c] = 0.0;
-      if (j0 + r < cend && c < kcw) cp8(&Pj[r * LDS + c], &A[(j0 + r) * n + k0 + kc + c]);
-      else Pj[r * LDS + c] = 0.0;
-    }
-    cp_wait();
-    __syncthreads();
-#pragma unroll 2
-    for (int c = 0; c < NB; ++c) {
-      double a[8], b[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) a[q] = Pi[(ty + 16 * q) * LDS + c];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) b[q] = Pj[(tx + 16 * q) * LDS + c];
-#pragma unroll
-      for (int x = 0; x < 8; ++x)
-#pragma unroll
-        for (int y = 0; y < 8; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+// 128 x 128 tiles of the trailing block.  Persistent CTAs (one per SM) walk the tile list; the
+// panel columns stream through shared memory in chunks of KC = 32 with the next chunk's
+// cp.async copies (possibly the next tile's) in flight while the current chunk is multiplied.
+// The products run on the fp64 tensor cores (DMMA m8n8k4, 256 FMAs per warp instruction; the
+// same 37 TF/s as the FMA pipe, but without the operand traffic that held an 8 x 8 register
+// outer product to ~45 %): 8 warps of 64 x 32 each, fp64 accumulators in registers.  The tile
+// is subtracted with fire-and-forget L2 reductions (RED.ADD.F64): every element has one owner
+// per launch and launches are stream-ordered, so this equals a read-modify-write bit for bit.
+constexpr int ST = 128;       // SYRK tile
+constexpr int KC = 32;        // panel columns per chunk
+constexpr int PLD = KC + 4;   // fp64 row stride of a staged chunk: fragment loads conflict-free
+constexpr int SYRK_SMEM = 2 * 2 * ST * PLD * (int)sizeof(double);  // 2 buffers x (rows i, rows j)
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+struct SyrkTiles {  // the lower tiles (ti >= tj, tj < Tj) in row-major order
+  int Ti, Tj;
+  __device__ int count() const {
+    const int tri = Tj * (Tj + 1) / 2;
+    return tri + (Ti - Tj) * Tj;
+  }
+  __device__ void at(int t, int& ti, int& tj) const {
+    const int tri = Tj * (Tj + 1) / 2;
+    if (t < tri) {
+      int r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+      while (r * (r + 1) / 2 > t) --r;
+      while ((r + 1) * (r + 2) / 2 <= t) ++r;
+      ti = r;
+      tj = t - r * (r + 1) / 2;
+    } else {
+      const int u = t - tri;
+      ti = Tj + u / Tj;
+      tj = u % Tj;
     }
   }
-  // A -= acc as fire-and-forget fp64 reductions in L2 (RED.ADD.F64): no load round trip on the
-  // SM; every element has exactly one owner per launch and launches are stream-ordered, so the
-  // result equals a read-modify-write bit for bit
-#pragma unroll
-  for (int x = 0; x < 8; ++x)
-#pragma unroll
-    for (int y = 0; y < 8; ++y) {
-      const int64_t i = i0 + ty + 16 * x, j = j0 + tx + 16 * y;
-      if (i < n && j <= i && j < cend) atomicAdd(&A[i * n + j], -acc[x][y]);
+};
+
+__global__ void __launch_bounds__(256, 1) syrk_trailing_kernel(double* __restrict__ A, int64_t n, int64_t k0,
+                                                               int kw, int64_t base, int64_t cend,
+                                                               SyrkTiles tl) {
+  extern __shared__ double syrk_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp & 1, wn = warp >> 1;  // warp tile: rows 64 wm + [0, 64), cols 32 wn + [0, 32)
+  const int gr = lane >> 2, gk = lane & 3;  // fragment row / k (A, B) and row / column pair (C)
+  const int ntiles = tl.count();
+  const int nch = (kw + KC - 1) / KC;
+  const int mytiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = mytiles * nch;  // this CTA's chunk sequence: (tile u, chunk kc)
+  // stage chunk g of the sequence into buffer g & 1 (16-byte copies when rows allow: n even,
+  // k0 even; else 8-byte copies)
+  const bool vec = ((n | k0) & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+  auto issue = [&](int g) {
+    const int u = g / nch, kc = (g % nch) * KC;
+    int ti, tj;
+    tl.at((int)blockIdx.x + u * (int)gridDim.x, ti, tj);
+    const int64_t i0 = base + (int64_t)ti * ST, j0 = base + (int64_t)tj * ST;
+    const int kcw = min(KC, kw - kc);
+    double* Pi = syrk_smem + (g & 1) * (2 * ST * PLD);
+    double* Pj = Pi + ST * PLD;
+    if (vec && kcw == KC) {
+#pragma unroll 1
+      for (int e = threadIdx.x; e < ST * KC / 2; e += 256) {
+        const int r = e >> 4, c = (e & 15) * 2;
+        if (i0 + r < n) cp16(&Pi[r * PLD + c], &A[(i0 + r) * n + k0 + kc + c]);
+        else *reinterpret_cast<double2*>(&Pi[r * PLD + c]) = make_double2(0.0, 0.0);
+        if (j0 + r < cend) cp16(&Pj[r * PLD + c], &A[(j0 + r) * n + k0 + kc + c]);
+        else *reinterpret_cast<double2*>(&Pj[r * PLD + c]) = make_double2(0.0, 0.0);
+      }
+    } else {
+      for (int e = threadIdx.x; e < ST * KC; e += 256) {
+        const int r = e / KC, c = e % KC;
+        if (i0 + r < n && c < kcw) cp8(&Pi[r * PLD + c], &A[(i0 + r) * n + k0 + kc + c]);
+        else Pi[r * PLD + c] = 0.0;
+        if (j0 + r < cend && c < kcw) cp8(&Pj[r * PLD + c], &A[(j0 + r) * n + k0 + kc + c]);
+        else Pj[r * PLD + c] = 0.0;
+      }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[8][4][2];
+#pragma unroll
+  for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+    for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+  if (total > 0) issue(0);
+  for (int g = 0; g < total; ++g) {
+    if (g + 1 < total) {
+      issue(g + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* Pi = syrk_smem + (g & 1) * (2 * ST * PLD) + (64 * wm + gr) * PLD + gk;
+    const double* Pj = syrk_smem + (g & 1) * (2 * ST * PLD) + ST * PLD + (32 * wn + gr) * PLD + gk;
+#pragma unroll 2
+    for (int ks = 0; ks < KC; ks += 4) {
+      double a[8], b[4];
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb) a[mb] = Pi[mb * 8 * PLD + ks];
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb) b[nb] = Pj[nb * 8 * PLD + ks];
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) dmma884(acc[mb][nb], a[mb], b[nb]);
+    }
+    if (g % nch == nch - 1) {
+      int ti, tj;
+      tl.at((int)blockIdx.x + (g / nch) * (int)gridDim.x, ti, tj);
+      const int64_t t_i0 = base + (int64_t)ti * ST, t_j0 = base + (int64_t)tj * ST;
+      const int64_t i0 = t_i0 + 64 * wm + gr, j0 = t_j0 + 32 * wn + 2 * gk;
+      const bool interior = ti > tj && t_i0 + ST <= n && t_j0 + ST <= cend;
+#pragma unroll
+      for (int mb = 0; mb < 8; ++mb) {
+        const int64_t i = i0 + 8 * mb;
+        double* row = A + i * n + j0;
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t j = j0 + 8 * nb + h;
+            if (interior || (i < n && j <= i && j < cend)) atomicAdd(row + 8 * nb + h, -acc[mb][nb][h]);
+            acc[mb][nb][h] = 0.0;
+          }
+      }
+    }
+    __syncthreads();  // buffer g & 1 is free for chunk g + 2
+  }
 }
 
 __global__ void zero_upper_kernel(double* __restrict__ A, int64_t n) {
@@ -297,7 +383,7 @@ LookAhead& look_ahead() {
 }
 
 ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket, cudaStream_t st) {
-  constexpr int kSyrkSmem = 2 * ST * LDS * sizeof(double);
+  constexpr int kSyrkSmem = SYRK_SMEM;
   GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
   auto panel = [&](int64_t k0, cudaStream_t ps) -> ganq_status_t {
@@ -307,9 +393,18 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket
     GANQ_LAUNCH_CHECK("panel_factor_kernel");
     return GANQ_OK;
   };
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   auto syrk = [&](int64_t k0, int kw, int64_t base, int64_t cend) -> ganq_status_t {
-    const unsigned Ti = (unsigned)((n - base + ST - 1) / ST), Tj = (unsigned)((cend - base + ST - 1) / ST);
-    syrk_trailing_kernel<<<dim3(Tj, Ti), 256, kSyrkSmem, st>>>(A, n, k0, kw, base, cend);
+    SyrkTiles tl;
+    tl.Ti = (int)((n - base + ST - 1) / ST);
+    tl.Tj = (int)((cend - base + ST - 1) / ST);
+    const int tiles = tl.Tj * (tl.Tj + 1) / 2 + (tl.Ti - tl.Tj) * tl.Tj;
+    syrk_trailing_kernel<<<(unsigned)min(tiles, sms), 256, kSyrkSmem, st>>>(A, n, k0, kw, base, cend, tl);
     GANQ_LAUNCH_CHECK("syrk_trailing_kernel");
     return GANQ_OK;
   };
