@@ -10,12 +10,13 @@ Public API (torch CUDA tensors; thin binding of include/ganq.h):
     pack_codes / codebook_f16 / lut_gemm   NEXT-1: N-bit storage and LUT mpGEMM (Fig. 1a)
     outlier_split / sparse_gemm_add        NEXT-2: GANQ* decomposition (Algorithm 2)
     kmeans_codebook                        NEXT-4: k-means T^0 (quantize_layer(init="kmeans"))
+    quantize_stacked                       NEXT-3: linears sharing H (q/k/v, gate/up) solved as one
 """
 from .api import (codebook_f16, factor, kmeans_codebook, hessian, lut_gemm, objective, objective_workspace_size, outlier_split,
-                  pack_codes, quantize_layer, sparse_gemm_add, tstep, version, workspace_size)
+                  pack_codes, quantize_layer, quantize_stacked, sparse_gemm_add, tstep, version, workspace_size)
 from ._lib import GanqError, NotPositiveDefinite
 
 __all__ = ["hessian", "quantize_layer", "objective", "tstep", "factor", "workspace_size",
            "objective_workspace_size", "version", "pack_codes", "codebook_f16", "lut_gemm", "outlier_split",
-           "sparse_gemm_add", "kmeans_codebook", "GanqError",
+           "sparse_gemm_add", "kmeans_codebook", "quantize_stacked", "GanqError",
            "NotPositiveDefinite"]

@@ -139,6 +139,33 @@ def quantize_layer(W: torch.Tensor, H: torch.Tensor, n_bits: int, iters: int = 1
     return Q, T
 
 
+def quantize_stacked(Ws, H: torch.Tensor, n_bits: int, iters: int = 10, *, T0=None, trace: bool = False,
+                     stream=None, **kw):
+    """Linears that read the same input (q/k/v, gate/up) share H = X X^T and so
+    its factor L: their weights are stacked row-wise into one problem, solved once (one
+    preconditioning + factorisation, one W H GEMM, one launch sequence per iteration) and split
+    back.  Eq. (4) decomposes the objective over rows and every GPU kernel is row-local
+    (per-row scales, row groups), so each block's (Q, T) equals a separate quantize_layer call
+    bit for bit (tests/test_gpu_pipeline.py).  Returns [(Q_i, T_i)] as views of the stacked
+    outputs (plus the stacked objective trace when trace=True)."""
+    Ws = list(Ws)
+    if not Ws:
+        raise ValueError("quantize_stacked: need at least one weight matrix")
+    n = H.shape[0]
+    for k, W in enumerate(Ws):
+        _need(W, torch.float32, 2, f"Ws[{k}]")
+        if W.shape[1] != n or W.device != Ws[0].device:
+            raise ValueError(f"quantize_stacked: Ws[{k}] is {tuple(W.shape)} on {W.device}; need (*, {n}) on "
+                             f"{Ws[0].device}")
+    rows = [W.shape[0] for W in Ws]
+    W = Ws[0] if len(Ws) == 1 else torch.cat(Ws, 0)
+    if T0 is not None and not isinstance(T0, torch.Tensor):
+        T0 = torch.cat(list(T0), 0)
+    res = quantize_layer(W, H, n_bits, iters, T0=T0, trace=trace, stream=stream, **kw)
+    out = list(zip(res[0].split(rows, 0), res[1].split(rows, 0)))
+    return (out, res[2]) if trace else out
+
+
 def objective(W, Q, T, H, per_row: bool = False, stream=None):
     """Eq. (1) via Eq. (8) on raw H; returns a Python float (and the fp64 per-row tensor)."""
     _need(W, torch.float32, 2, "W")

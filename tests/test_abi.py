@@ -116,3 +116,26 @@ def test_packed_row_bytes(lib):
 def test_pipeline_module_imports():
     from paper_2501_12956_b200 import pipeline
     assert hasattr(pipeline, "LayerPipeline") and hasattr(pipeline, "quantize_layers")
+
+
+def test_checkpoint_plan_and_files(tmp_path):
+    import torch
+    from paper_2501_12956_b200 import pipeline as pl
+    assert pl.checkpoint_plan(3, None) == ([], [0, 1, 2])
+    meta = {"m": 2, "n": 4, "n_bits": 2, "iters": 1}
+    pl.save_checkpoint(str(tmp_path), 1, torch.zeros((2, 4), dtype=torch.uint8), torch.ones((2, 4)), meta)
+    assert pl.checkpoint_plan(3, str(tmp_path)) == ([1], [0, 2])
+    Q, T = pl.load_checkpoint(str(tmp_path), 1, meta)
+    assert Q.dtype == torch.uint8 and torch.equal(T, torch.ones((2, 4)))
+    with pytest.raises(ValueError):
+        pl.load_checkpoint(str(tmp_path), 1, {**meta, "iters": 2})
+    assert not any(f.name.endswith(".tmp") for f in tmp_path.iterdir())
+
+
+def test_quantize_stacked_validates_without_gpu():
+    import torch
+    import paper_2501_12956_b200 as g
+    with pytest.raises(ValueError):
+        g.quantize_stacked([], torch.zeros((4, 4), dtype=torch.float64), 2)
+    with pytest.raises(ValueError, match="CUDA"):
+        g.quantize_stacked([torch.zeros((2, 4))], torch.zeros((4, 4), dtype=torch.float64), 2)
