@@ -132,16 +132,17 @@ def cores():
 
 
 # --------------------------------------------------------------------------- our arm
-def stage_roofline(name, ms, launches, m, n, p, K, peaks, world):
+def stage_roofline(name, ms, launches, m, n, p, K, peaks, world, nlev=16):
     """Algorithmic work of a stage per step against the peak of the unit it runs on
     (DESIGN.md 'Roofline accounting').  Effective peaks of the tensor-core formulations:
     tf32x3 (sstep, gemm_wh) = tf32 peak / 3 passes, tf32 = bf16 / 2 (nominal ratio);
-    tgram = int8 MAC rate / 48 MACs per algorithmic addition (16 one-hot levels x 3 digits),
+    tgram = int8 MAC rate / (3 nlev) MACs per algorithmic addition (nlev one-hot levels x 3 digits:
+    48 at 4 bits, 24 at 3 bits),
     int8 = 2 x bf16 (nominal ratio).  bf16 is the measured sustained cuBLAS figure."""
     clk = peaks["sm_mhz"] * 1e6
     fp64 = 148 * 64 * 2 * clk / 1e12           # fp64 FMA, TFLOP/s
     tf32x3 = peaks["bf16_sus"] / 2 / 3          # fp32-accurate tensor-core flop/s, TFLOP/s
-    tgram_peak = peaks["bf16_sus"] / 48         # int8 MAC/s (= bf16 flop/s) / 48 -> additions/s
+    tgram_peak = peaks["bf16_sus"] / (3 * nlev)  # int8 MAC/s (= bf16 flop/s) / (3 nlev) -> additions/s
     s = ms / 1e3
     if s <= 0:
         return None
@@ -150,7 +151,7 @@ def stage_roofline(name, ms, launches, m, n, p, K, peaks, world):
     elif name == "tgram":
         work, unit, bound, peak = K * m * n * (n - 1) / 2 / 1e12, "TFLOP/s", "tensor", tgram_peak
     elif name == "tsolve":
-        work, unit, bound, peak = K * (5.0 * m * n + 4 * 8 * m * 256) / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
+        work, unit, bound, peak = K * (5.0 * m * n + 4 * 8 * m * nlev * nlev) / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
     elif name == "sstep":
         work, unit, bound, peak = K * m * n * (n - 1) / 1e12, "TFLOP/s", "tensor", tf32x3
     elif name == "gemm_wh":
@@ -246,7 +247,7 @@ def run_ours(args):
         if ms_arr[i] <= 0:
             continue
         ms_i = ms_arr[i] / args.steps
-        rl = stage_roofline(name, ms_i, ln_arr[i] / args.steps, ml, n, t1 - t0, K, peaks, world)
+        rl = stage_roofline(name, ms_i, ln_arr[i] / args.steps, ml, n, t1 - t0, K, peaks, world, 1 << nbits)
         stages[name] = rl if rl else dict(ms=round(ms_i, 4), launches=int(ln_arr[i] / args.steps))
     dominant = max((k for k in stages if "frac" in stages[k]), key=lambda k: stages[k]["ms"])
     roof = {k: stages[dominant][k] for k in ("bound", "achieved", "peak", "unit", "frac")}

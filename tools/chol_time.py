@@ -1,7 +1,8 @@
 """Time ganq_factor (precondition + blocked fp64 Cholesky) on a synthetic H at n = 4096 / 11008.
 
-    python tools/chol_time.py [n ...]
+    python tools/chol_time.py [n ...]      (CHOL_TOKENS=p overrides the 4 n calibration tokens)
 """
+import os
 import sys
 
 import torch
@@ -11,7 +12,7 @@ import synthetic
 import paper_2501_12956_b200 as g
 
 for n in [int(a) for a in sys.argv[1:]] or [4096]:
-    X = synthetic.make_activations(4 * n, n, seed=2000, device="cuda")
+    X = synthetic.make_activations(int(os.environ.get("CHOL_TOKENS", 4 * n)), n, seed=2000, device="cuda")
     H = g.hessian(X)
     del X
     for _ in range(2):
