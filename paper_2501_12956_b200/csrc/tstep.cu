@@ -48,6 +48,39 @@ trhs_kernel(const double* __restrict__ hdiag, const float* __restrict__ WH, cons
       sC[warp][a][lane] += 1;
     }
   };
+  // two columns per read-modify-write round: both slots are loaded before either is stored
+  // (the chain through shared memory is per pair, not per column); equal codes add in column
+  // order, exactly as two successive add() calls
+  auto add2 = [&](int a1, double h1, float r1, int a2, double h2, float r2) {
+    const bool v1 = a1 < NLEV, v2 = a2 < NLEV, same = a1 == a2;
+    const int b1 = v1 ? a1 : 0, b2 = v2 ? a2 : 0;
+    double D1 = sD[warp][b1][lane], R1 = sR[warp][b1][lane];
+    double D2 = sD[warp][b2][lane], R2 = sR[warp][b2][lane];
+    int C1 = sC[warp][b1][lane], C2 = sC[warp][b2][lane];
+    if (v1) {
+      D1 += h1;
+      R1 += (double)r1;
+      C1 += 1;
+      if (same) {
+        D1 += h2;
+        R1 += (double)r2;
+        C1 += 1;
+      }
+    }
+    if (v2 && !same) {
+      D2 += h2;
+      R2 += (double)r2;
+      C2 += 1;
+      sD[warp][b2][lane] = D2;
+      sR[warp][b2][lane] = R2;
+      sC[warp][b2][lane] = C2;
+    }
+    if (v1) {
+      sD[warp][b1][lane] = D1;
+      sR[warp][b1][lane] = R1;
+      sC[warp][b1][lane] = C1;
+    }
+  };
   int64_t j0 = 0;
   if ((n & 3) == 0) {
     // lane takes 4 consecutive columns per 128-column step; two steps of loads in flight
@@ -65,10 +98,8 @@ trhs_kernel(const double* __restrict__ hdiag, const float* __restrict__ WH, cons
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        add(qv[u] & 255, h0[u].x, wv[u].x);
-        add((qv[u] >> 8) & 255, h0[u].y, wv[u].y);
-        add((qv[u] >> 16) & 255, h1[u].x, wv[u].z);
-        add(qv[u] >> 24, h1[u].y, wv[u].w);
+        add2(qv[u] & 255, h0[u].x, wv[u].x, (qv[u] >> 8) & 255, h0[u].y, wv[u].y);
+        add2((qv[u] >> 16) & 255, h1[u].x, wv[u].z, qv[u] >> 24, h1[u].y, wv[u].w);
       }
     }
   }
@@ -112,17 +143,33 @@ tsolve_kernel(double* __restrict__ G, const double* __restrict__ Dv, const doubl
   double g[NLEV];
   double maxdiag = 0.0;
   // assemble G = C + C^T + D; C (strict lower sums j > k) arrives as GANQ_TGRAM_SPLIT
-  // partials (j-tile ranges, tgram_tc.cu) stacked along m, added in fixed order
+  // partials (j-tile ranges, tgram_tc.cu) stacked along m, added in fixed order.  The warp's
+  // RPW rows are contiguous in every partial: coalesced 16-byte loads, all in flight together,
+  // summed into shared memory, then read per (l, c) and (c, l)
+  __shared__ double sC[8][32 * NLEV];
   const size_t pstride = (size_t)m * NLEV * NLEV;
+  {
+    const int64_t wrow0 = ((int64_t)blockIdx.x * 8 + warp) * RPW;
+    const int64_t nrow = m - wrow0 < RPW ? m - wrow0 : RPW;
+    const int total = nrow > 0 ? (int)nrow * NLEV * NLEV : 0;
+    const double* src = G + wrow0 * NLEV * NLEV;
+#pragma unroll 4
+    for (int e = 2 * lane; e < total; e += 64) {
+      double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int c = 0; c < NLEV; ++c) {
-    double clc = 0.0, ccl = 0.0;
-    for (int p = 0; p < kTgramSplit; ++p) {
-      clc += G[p * pstride + (rw * NLEV + l) * NLEV + c];
-      ccl += G[p * pstride + (rw * NLEV + c) * NLEV + l];
+      for (int p = 0; p < kTgramSplit; ++p) {
+        const double2 v = *reinterpret_cast<const double2*>(src + p * pstride + e);
+        acc.x += v.x;
+        acc.y += v.y;
+      }
+      sC[warp][e] = acc.x;
+      sC[warp][e + 1] = acc.y;
     }
-    g[c] = clc + ccl + (c == l ? Dv[rw * NLEV + l] : 0.0);
+    __syncwarp();
   }
+  const double* cw = &sC[warp][seg * NLEV * NLEV];
+#pragma unroll
+  for (int c = 0; c < NLEV; ++c) g[c] = cw[l * NLEV + c] + cw[c * NLEV + l] + (c == l ? Dv[rw * NLEV + l] : 0.0);
   __syncwarp();
   if (live) {
 #pragma unroll
