@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(PF_THREADS) panel_factor_kernel(double* __rest
 constexpr int ST = 128;       // SYRK tile
 constexpr int KC = 32;        // panel columns per chunk
 constexpr int PLD = KC + 4;   // fp64 row stride of a staged chunk: fragment loads conflict-free
-constexpr int SYRK_SMEM = 2 * 2 * ST * PLD * (int)sizeof(double);  // 2 buffers x (rows i, rows j)
+constexpr int SYRK_SMEM = 2 * 2 * ST * PLD * (int)sizeof(double);  // 2 buffers x (rows i, rows j), 128 x 128
+constexpr int SYRK_SMEM_THIN = 2 * 2 * 64 * PLD * (int)sizeof(double);  // 64 x 64
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -230,12 +231,18 @@ struct SyrkTiles {  // the lower tiles (ti >= tj, tj < Tj) in row-major order
   }
 };
 
+// TI x TJ tiles (128 x 128 for the bulk update; 64 x 64 for the thin update of the next panel's
+// 64 columns, twice the CTAs and none of the masked half-tile work); 8 warps as 2 (rows) x 4
+// (columns), each TI/2 x TJ/4 = MB x NBB blocks of 8 x 8.
+template <int TI, int TJ>
 __global__ void __launch_bounds__(256, 1) syrk_trailing_kernel(double* __restrict__ A, int64_t n, int64_t k0,
                                                                int kw, int64_t base, int64_t cend,
                                                                SyrkTiles tl) {
+  constexpr int MB = TI / 16, NBB = TJ / 32;
+  constexpr int BUF = (TI + TJ) * PLD;  // one buffer: rows i, then rows j
   extern __shared__ double syrk_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp & 1, wn = warp >> 1;  // warp tile: rows 64 wm + [0, 64), cols 32 wn + [0, 32)
+  const int wm = warp & 1, wn = warp >> 1;  // warp tile: rows (TI/2) wm + [0, TI/2), cols (TJ/4) wn + ...
   const int gr = lane >> 2, gk = lane & 3;  // fragment row / k (A, B) and row / column pair (C)
   const int ntiles = tl.count();
   const int nch = (kw + KC - 1) / KC;
@@ -248,35 +255,41 @@ __global__ void __launch_bounds__(256, 1) syrk_trailing_kernel(double* __restric
     const int u = g / nch, kc = (g % nch) * KC;
     int ti, tj;
     tl.at((int)blockIdx.x + u * (int)gridDim.x, ti, tj);
-    const int64_t i0 = base + (int64_t)ti * ST, j0 = base + (int64_t)tj * ST;
+    const int64_t i0 = base + (int64_t)ti * TI, j0 = base + (int64_t)tj * TJ;
     const int kcw = min(KC, kw - kc);
-    double* Pi = syrk_smem + (g & 1) * (2 * ST * PLD);
-    double* Pj = Pi + ST * PLD;
+    double* Pi = syrk_smem + (g & 1) * BUF;
+    double* Pj = Pi + TI * PLD;
     if (vec && kcw == KC) {
 #pragma unroll 1
-      for (int e = threadIdx.x; e < ST * KC / 2; e += 256) {
+      for (int e = threadIdx.x; e < TI * KC / 2; e += 256) {
         const int r = e >> 4, c = (e & 15) * 2;
         if (i0 + r < n) cp16(&Pi[r * PLD + c], &A[(i0 + r) * n + k0 + kc + c]);
         else *reinterpret_cast<double2*>(&Pi[r * PLD + c]) = make_double2(0.0, 0.0);
+      }
+#pragma unroll 1
+      for (int e = threadIdx.x; e < TJ * KC / 2; e += 256) {
+        const int r = e >> 4, c = (e & 15) * 2;
         if (j0 + r < cend) cp16(&Pj[r * PLD + c], &A[(j0 + r) * n + k0 + kc + c]);
         else *reinterpret_cast<double2*>(&Pj[r * PLD + c]) = make_double2(0.0, 0.0);
       }
     } else {
-      for (int e = threadIdx.x; e < ST * KC; e += 256) {
+      for (int e = threadIdx.x; e < (TI + TJ) * KC; e += 256) {
         const int r = e / KC, c = e % KC;
-        if (i0 + r < n && c < kcw) cp8(&Pi[r * PLD + c], &A[(i0 + r) * n + k0 + kc + c]);
-        else Pi[r * PLD + c] = 0.0;
-        if (j0 + r < cend && c < kcw) cp8(&Pj[r * PLD + c], &A[(j0 + r) * n + k0 + kc + c]);
-        else Pj[r * PLD + c] = 0.0;
+        const bool isi = r < TI;
+        const int rr = isi ? r : r - TI;
+        const int64_t gr0 = isi ? i0 + rr : j0 + rr;
+        double* dst = (isi ? Pi : Pj) + rr * PLD + c;
+        if (gr0 < (isi ? n : cend) && c < kcw) cp8(dst, &A[gr0 * n + k0 + kc + c]);
+        else *dst = 0.0;
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  double acc[8][4][2];
+  double acc[MB][NBB][2];
 #pragma unroll
-  for (int mb = 0; mb < 8; ++mb)
+  for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < 4; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
+    for (int nb = 0; nb < NBB; ++nb) acc[mb][nb][0] = acc[mb][nb][1] = 0.0;
   if (total > 0) issue(0);
   for (int g = 0; g < total; ++g) {
     if (g + 1 < total) {
@@ -286,32 +299,32 @@ __global__ void __launch_bounds__(256, 1) syrk_trailing_kernel(double* __restric
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    const double* Pi = syrk_smem + (g & 1) * (2 * ST * PLD) + (64 * wm + gr) * PLD + gk;
-    const double* Pj = syrk_smem + (g & 1) * (2 * ST * PLD) + ST * PLD + (32 * wn + gr) * PLD + gk;
+    const double* Pi = syrk_smem + (g & 1) * BUF + ((TI / 2) * wm + gr) * PLD + gk;
+    const double* Pj = syrk_smem + (g & 1) * BUF + TI * PLD + ((TJ / 4) * wn + gr) * PLD + gk;
 #pragma unroll 2
     for (int ks = 0; ks < KC; ks += 4) {
-      double a[8], b[4];
+      double a[MB], b[NBB];
 #pragma unroll
-      for (int mb = 0; mb < 8; ++mb) a[mb] = Pi[mb * 8 * PLD + ks];
+      for (int mb = 0; mb < MB; ++mb) a[mb] = Pi[mb * 8 * PLD + ks];
 #pragma unroll
-      for (int nb = 0; nb < 4; ++nb) b[nb] = Pj[nb * 8 * PLD + ks];
+      for (int nb = 0; nb < NBB; ++nb) b[nb] = Pj[nb * 8 * PLD + ks];
 #pragma unroll
-      for (int mb = 0; mb < 8; ++mb)
+      for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-        for (int nb = 0; nb < 4; ++nb) dmma884(acc[mb][nb], a[mb], b[nb]);
+        for (int nb = 0; nb < NBB; ++nb) dmma884(acc[mb][nb], a[mb], b[nb]);
     }
     if (g % nch == nch - 1) {
       int ti, tj;
       tl.at((int)blockIdx.x + (g / nch) * (int)gridDim.x, ti, tj);
-      const int64_t t_i0 = base + (int64_t)ti * ST, t_j0 = base + (int64_t)tj * ST;
-      const int64_t i0 = t_i0 + 64 * wm + gr, j0 = t_j0 + 32 * wn + 2 * gk;
-      const bool interior = ti > tj && t_i0 + ST <= n && t_j0 + ST <= cend;
+      const int64_t t_i0 = base + (int64_t)ti * TI, t_j0 = base + (int64_t)tj * TJ;
+      const int64_t i0 = t_i0 + (TI / 2) * wm + gr, j0 = t_j0 + (TJ / 4) * wn + 2 * gk;
+      const bool interior = t_i0 >= t_j0 + TJ && t_i0 + TI <= n && t_j0 + TJ <= cend;
 #pragma unroll
-      for (int mb = 0; mb < 8; ++mb) {
+      for (int mb = 0; mb < MB; ++mb) {
         const int64_t i = i0 + 8 * mb;
         double* row = A + i * n + j0;
 #pragma unroll
-        for (int nb = 0; nb < 4; ++nb)
+        for (int nb = 0; nb < NBB; ++nb)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int64_t j = j0 + 8 * nb + h;
@@ -384,7 +397,9 @@ LookAhead& look_ahead() {
 
 ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket, cudaStream_t st) {
   constexpr int kSyrkSmem = SYRK_SMEM;
-  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel,
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SYRK_SMEM_THIN));
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<ST, ST>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
   auto panel = [&](int64_t k0, cudaStream_t ps) -> ganq_status_t {
     const int64_t rest = n - k0 - NB;
@@ -401,10 +416,17 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket
   }
   auto syrk = [&](int64_t k0, int kw, int64_t base, int64_t cend) -> ganq_status_t {
     SyrkTiles tl;
-    tl.Ti = (int)((n - base + ST - 1) / ST);
-    tl.Tj = (int)((cend - base + ST - 1) / ST);
-    const int tiles = tl.Tj * (tl.Tj + 1) / 2 + (tl.Ti - tl.Tj) * tl.Tj;
-    syrk_trailing_kernel<<<(unsigned)min(tiles, sms), 256, kSyrkSmem, st>>>(A, n, k0, kw, base, cend, tl);
+    if (cend - base <= 64 && (n - base + 63) / 64 <= sms) {  // thin: the next panel's 64 columns, one wave
+      tl.Ti = (int)((n - base + 63) / 64);
+      tl.Tj = 1;
+      syrk_trailing_kernel<64, 64><<<(unsigned)min(tl.Ti, sms), 256, SYRK_SMEM_THIN, st>>>(A, n, k0, kw, base,
+                                                                                         cend, tl);
+    } else {
+      tl.Ti = (int)((n - base + ST - 1) / ST);
+      tl.Tj = (int)((cend - base + ST - 1) / ST);
+      const int tiles = tl.Tj * (tl.Tj + 1) / 2 + (tl.Ti - tl.Tj) * tl.Tj;
+      syrk_trailing_kernel<ST, ST><<<(unsigned)min(tiles, sms), 256, kSyrkSmem, st>>>(A, n, k0, kw, base, cend, tl);
+    }
     GANQ_LAUNCH_CHECK("syrk_trailing_kernel");
     return GANQ_OK;
   };
