@@ -25,6 +25,10 @@
  *    thread-local message.  On error, outputs are unspecified.
  *  - Rows are independent (Eq. 2): a row shard is W + r0*n with
  *    m = m_local; multi-GPU needs no further entry point.
+ *  - Non-finite inputs (Inf / NaN in X, W or H) are undefined behaviour.  With the
+ *    environment variable GANQ_VALIDATE=1, ganq_hessian and ganq_quantize_layer scan
+ *    their inputs first, synchronise, and return GANQ_ERR_INVALID_ARG naming the first
+ *    non-finite element (ganq_last_error_index() = its flat index).
  */
 #ifndef GANQ_H_
 #define GANQ_H_

@@ -373,6 +373,10 @@ ganq_status_t ganq_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, i
     return GANQ_ERR_INVALID_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if (validate_enabled()) {
+    ganq_status_t s = validate_finite_bf16(X, p, n, "X", st);
+    if (s) return s;
+  }
   GANQ_STAGE(ST_HESSIAN);
   return launch_hessian(X, p, n, H, accumulate, st);
 }
@@ -409,6 +413,10 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
   }
   cudaStream_t st = (cudaStream_t)stream;
   void* ws = workspace;
+  if (validate_enabled()) {
+    if ((s = validate_finite_f32(W, m, n, "W", st))) return s;
+    if ((s = validate_finite_f64(H, n, n, "H", st))) return s;
+  }
   // H' = precondition(H), L = Cholesky(H')   (App. A / Remark 1, Eq. 9)
   if ((s = factor(H, n, o, ws, L, nullptr, st))) return s;
   float* Lhat = at<float>(ws, L.Lhat);

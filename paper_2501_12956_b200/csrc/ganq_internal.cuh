@@ -11,6 +11,12 @@ namespace ganq {
 // ---------------------------------------------------------------- error state
 void set_error(ganq_status_t st, const char* fmt, ...);
 void set_error_index(int64_t idx);
+// validate.cu: GANQ_VALIDATE=1 scans inputs for Inf / NaN (synchronises; INVALID_ARG on a hit)
+bool validate_enabled();
+ganq_status_t validate_finite_f32(const float* x, int64_t rows, int64_t cols, const char* what, cudaStream_t st);
+ganq_status_t validate_finite_f64(const double* x, int64_t rows, int64_t cols, const char* what, cudaStream_t st);
+ganq_status_t validate_finite_bf16(const uint16_t* x, int64_t rows, int64_t cols, const char* what,
+                                   cudaStream_t st);
 ganq_status_t cuda_fail(cudaError_t e, const char* where);
 
 #define GANQ_CUDA_TRY(expr)                                   \

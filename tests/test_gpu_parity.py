@@ -370,3 +370,25 @@ def test_precond_auto_policy():
     Qa2, Ta2 = g.quantize_layer(W.to(DEV), H2, 3, 2, precond="auto")
     Qd2, Td2 = g.quantize_layer(W.to(DEV), H2, 3, 2, precond="adaptive")
     assert torch.equal(Qa2, Qd2) and torch.equal(Ta2, Td2)
+
+
+def test_validate_nonfinite_inputs(monkeypatch):
+    """GANQ_VALIDATE=1: non-finite X / W / H are refused with the first offending element."""
+    W, X = make_case(8, 64, 256, seed=5)
+    W, X = W.to(DEV), X.to(DEV)
+    H = gpu_H(X)
+    Wb = W.clone()
+    Wb[3, 17] = float("nan")
+    Xb = X.clone()
+    Xb[10, 5] = float("inf")
+    Hb = H.clone()
+    Hb[2, 7] = float("inf")
+    monkeypatch.setenv("GANQ_VALIDATE", "1")
+    with pytest.raises(g.GanqError) as ei:
+        g.quantize_layer(Wb, H, 3, 1)
+    assert "W at (3, 17)" in str(ei.value) and ei.value.index == 3 * 64 + 17
+    with pytest.raises(g.GanqError, match="H at \\(2, 7\\)"):
+        g.quantize_layer(W, Hb, 3, 1)
+    with pytest.raises(g.GanqError, match="X at \\(10, 5\\)"):
+        g.hessian(Xb)
+    g.quantize_layer(W, H, 3, 1)  # clean inputs pass
