@@ -172,13 +172,11 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         const int jb = (int)(n - (int64_t)PW * (q + 1));
         const int jbs = jb + (int)(np - n);  // fp32 Lhat storage column of the panel start
         for (int qs = 0; qs < q; ++qs) {
-          if (qs == q - 1) {
-            TP_T0(t1);
-            mbar_wait(&sm.ebar, (uint32_t)((q - 1) & 1));  // panel q-1 residuals written
-            TP_ACC(w_ebar, t1);
-            mbar_arrive_expect_tx(&sm.ldbar, PW * PW * 4);  // ... and its Ld no longer read
-            tma_load_2d(&sm.Ld[0][0], &tmLd, &sm.ldbar, jbs, jb);
-          }
+          // the newest source panel: its LhatT quarters go out (multicast) before this CTA's
+          // residuals exist -- they depend on L only -- so a peer's stage is not held back by
+          // this CTA's decisions; only the E digit tiles wait for ebar
+          const bool newest = (qs == q - 1);
+          const uint32_t kb0 = kb;
           for (int k2 = 0; k2 < PW / UB; ++k2, ++kb) {
             const int u0 = (int)(npq - (int64_t)PW * (qs + 1)) + k2 * UB;  // int8 storage column
             const uint32_t s = kb % STAGES;
@@ -192,7 +190,22 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
               tma_load_3d_mc(st + d * A_TILE + sl * UB, &tmLT, &sm.full[s], u0, jb + sl, d, CMASK);
-              tma_load_3d(st + 3 * A_TILE + d * B_TILE, &tmE, &sm.full[s], u0, (int)r0, d);
+              if (!newest) tma_load_3d(st + 3 * A_TILE + d * B_TILE, &tmE, &sm.full[s], u0, (int)r0, d);
+            }
+          }
+          if (newest) {
+            TP_T0(t1);
+            mbar_wait(&sm.ebar, (uint32_t)((q - 1) & 1));  // panel q-1 residuals written
+            TP_ACC(w_ebar, t1);
+            mbar_arrive_expect_tx(&sm.ldbar, PW * PW * 4);  // ... and its Ld no longer read
+            tma_load_2d(&sm.Ld[0][0], &tmLd, &sm.ldbar, jbs, jb);
+            for (int k2 = 0; k2 < PW / UB; ++k2) {
+              const int u0 = (int)(npq - (int64_t)PW * (qs + 1)) + k2 * UB;
+              const uint32_t s = (kb0 + k2) % STAGES;
+              uint8_t* st = tiles + s * STAGE_BYTES;
+#pragma unroll
+              for (int d = 0; d < 3; ++d)
+                tma_load_3d(st + 3 * A_TILE + d * B_TILE, &tmE, &sm.full[s], u0, (int)r0, d);
             }
           }
         }
