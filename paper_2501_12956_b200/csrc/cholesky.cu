@@ -200,8 +200,9 @@ __global__ void __launch_bounds__(PF_THREADS) panel_factor_kernel(double* __rest
 constexpr int ST = 128;       // SYRK tile
 constexpr int KC = 32;        // panel columns per chunk
 constexpr int PLD = KC + 4;   // fp64 row stride of a staged chunk: fragment loads conflict-free
-constexpr int SYRK_SMEM = 2 * 2 * ST * PLD * (int)sizeof(double);  // 2 buffers x (rows i, rows j), 128 x 128
+// shared memory: 2 buffers x (TI + TJ) rows x PLD
 constexpr int SYRK_SMEM_THIN = 2 * 2 * 64 * PLD * (int)sizeof(double);  // 64 x 64
+constexpr int SYRK_SMEM_BULK = 2 * (ST + 64) * PLD * (int)sizeof(double);  // 128 x 64
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -209,23 +210,25 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-struct SyrkTiles {  // the lower tiles (ti >= tj, tj < Tj) in row-major order
-  int Ti, Tj;
-  __device__ int count() const {
-    const int tri = Tj * (Tj + 1) / 2;
-    return tri + (Ti - Tj) * Tj;
+struct SyrkTiles {  // lower tiles in row-major order: row ti holds j-tiles tj < min(R (ti + 1), Tj)
+  int Ti, Tj, R;     // R = TI / TJ (1 or 2)
+  __host__ __device__ int tri_rows() const { return (Tj + R - 1) / R - 1; }  // rows with < Tj tiles
+  __host__ __device__ int cum(int r) const { return R * r * (r + 1) / 2; }  // tiles in rows < r (r <= tri_rows)
+  __host__ __device__ int count() const {
+    const int rt = Ti < tri_rows() ? Ti : tri_rows();
+    return cum(rt) + (Ti > rt ? (Ti - rt) * Tj : 0);
   }
   __device__ void at(int t, int& ti, int& tj) const {
-    const int tri = Tj * (Tj + 1) / 2;
-    if (t < tri) {
-      int r = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-      while (r * (r + 1) / 2 > t) --r;
-      while ((r + 1) * (r + 2) / 2 <= t) ++r;
+    const int rt = Ti < tri_rows() ? Ti : tri_rows();
+    if (t < cum(rt)) {
+      int r = (int)((sqrtf(8.0f * (float)t / (float)R + 1.0f) - 1.0f) * 0.5f);
+      while (r > 0 && cum(r) > t) --r;
+      while (cum(r + 1) <= t) ++r;
       ti = r;
-      tj = t - r * (r + 1) / 2;
+      tj = t - cum(r);
     } else {
-      const int u = t - tri;
-      ti = Tj + u / Tj;
+      const int u = t - cum(rt);
+      ti = rt + u / Tj;
       tj = u % Tj;
     }
   }
@@ -235,7 +238,7 @@ struct SyrkTiles {  // the lower tiles (ti >= tj, tj < Tj) in row-major order
 // 64 columns, twice the CTAs and none of the masked half-tile work); 8 warps as 2 (rows) x 4
 // (columns), each TI/2 x TJ/4 = MB x NBB blocks of 8 x 8.
 template <int TI, int TJ>
-__global__ void __launch_bounds__(256, 1) syrk_trailing_kernel(double* __restrict__ A, int64_t n, int64_t k0,
+__global__ void __launch_bounds__(256, TJ < 128 ? 2 : 1) syrk_trailing_kernel(double* __restrict__ A, int64_t n, int64_t k0,
                                                                int kw, int64_t base, int64_t cend,
                                                                SyrkTiles tl) {
   constexpr int MB = TI / 16, NBB = TJ / 32;
@@ -396,11 +399,10 @@ LookAhead& look_ahead() {
 }
 
 ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket, cudaStream_t st) {
-  constexpr int kSyrkSmem = SYRK_SMEM;
   GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      SYRK_SMEM_THIN));
-  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<ST, ST>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kSyrkSmem));
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<ST, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SYRK_SMEM_BULK));
   auto panel = [&](int64_t k0, cudaStream_t ps) -> ganq_status_t {
     const int64_t rest = n - k0 - NB;
     const unsigned grid = rest > 0 ? (unsigned)((rest + PR - 1) / PR) : 1u;
@@ -419,13 +421,16 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket
     if (cend - base <= 64 && (n - base + 63) / 64 <= sms) {  // thin: the next panel's 64 columns, one wave
       tl.Ti = (int)((n - base + 63) / 64);
       tl.Tj = 1;
+      tl.R = 1;
       syrk_trailing_kernel<64, 64><<<(unsigned)min(tl.Ti, sms), 256, SYRK_SMEM_THIN, st>>>(A, n, k0, kw, base,
                                                                                          cend, tl);
     } else {
+      // 128 x 64 tiles, two CTAs per SM: one CTA's loads and reductions overlap the other's MMAs
       tl.Ti = (int)((n - base + ST - 1) / ST);
-      tl.Tj = (int)((cend - base + ST - 1) / ST);
-      const int tiles = tl.Tj * (tl.Tj + 1) / 2 + (tl.Ti - tl.Tj) * tl.Tj;
-      syrk_trailing_kernel<ST, ST><<<(unsigned)min(tiles, sms), 256, kSyrkSmem, st>>>(A, n, k0, kw, base, cend, tl);
+      tl.Tj = (int)((cend - base + 63) / 64);
+      tl.R = 2;
+      syrk_trailing_kernel<ST, 64><<<(unsigned)min(tl.count(), 2 * sms), 256, SYRK_SMEM_BULK, st>>>(
+          A, n, k0, kw, base, cend, tl);
     }
     GANQ_LAUNCH_CHECK("syrk_trailing_kernel");
     return GANQ_OK;
