@@ -13,7 +13,10 @@
 // independent of summation order.
 //
 // Pipeline (one CTA per (row group, j range); SPLIT CTAs per group over balanced j ranges):
-//   warp 0     TMA: the three digit tiles of H (128 j x 64 k, SWIZZLE_64B) per stage
+//   warp 0     TMA: the three digit tiles of H (128 j x 128 k, SWIZZLE_128B) per stage; a stage
+//              of 128 k (12 MMAs) amortises the issuer's per-stage barrier wait and commit, which
+//              cost ~30 % of the MMA rate at 64 k (tools/micro/mma_rate.cu: a try_wait per 6 MMAs
+//              alone takes 64 -> 72 cycles per MMA)
 //   warp 1     MMA issuer (+TMEM owner): 3 int32 accumulators of 128 columns, A from TMEM
 //   warps 2-5  one-hot producers, one per TMEM lane quarter: lane (i,b) builds its 64 bytes
 //              [q_ik == b] per stage in registers and tcgen05.st's them into a TMEM ring
@@ -35,17 +38,17 @@ namespace ganq {
 namespace {
 
 constexpr int TJ = 128;          // j per tile (UMMA N)
-constexpr int TK = 64;           // k per stage (64-byte swizzle rows of int8)
-constexpr int STAGES = 6;
-constexpr int B_TILE = TJ * TK;                  // 8 KB digit tile of H
-constexpr int STAGE_BYTES = 3 * B_TILE;          // 24 KB (the one-hot A operand lives in TMEM)
+constexpr int TK = 128;          // k per stage (128-byte swizzle rows of int8)
+constexpr int STAGES = 3;
+constexpr int B_TILE = TJ * TK;                  // 16 KB digit tile of H
+constexpr int STAGE_BYTES = 3 * B_TILE;          // 48 KB (the one-hot A operand lives in TMEM)
 constexpr int SPLIT = 4;                         // CTAs per row group (balanced j ranges)
 constexpr int CS = 2;                            // cluster: CS row groups share every H tile
 constexpr uint16_t CMASK = (1u << CS) - 1;
 constexpr int SLICE = TJ / CS;                   // j rows of each digit tile one CTA loads
 constexpr int THREADS = 448;                     // 14 warps
 constexpr int A_COL0 = 3 * TJ;                   // TMEM: 3 accumulators, then the A ring
-constexpr int A_COLS = TK / 4;                   // 16 columns of 4 int8 per stage
+constexpr int A_COLS = TK / 4;                   // 32 columns of 4 int8 per stage
 constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile (sorting unit)
 constexpr uint32_t IDESC = umma_idesc_u8s8(128, TJ);  // A = one-hot bytes 0 / 128 (u8)
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
@@ -76,7 +79,7 @@ struct TcSmem {
 };
 
 __host__ __device__ inline int ktiles_of(int jt) { return (jt * TJ + TJ - 1) / TK + 1; }
-static_assert(TJ == 2 * TK, "producers step ktiles_of by TJ / TK = 2");
+static_assert(TJ % TK == 0, "producers step ktiles_of by TJ / TK");
 
 template <int NLEV>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -166,7 +169,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
             const uint32_t b_addr = s_addr + l * B_TILE;
 #pragma unroll
             for (int kk = 0; kk < TK / 32; ++kk)
-              if (!(dbg & 8)) mma_i8_ts(tmem + l * TJ, a_tmem + kk * 8, umma_desc_sw64(b_addr + kk * 32), IDESC,
+              if (!(dbg & 8)) mma_i8_ts(tmem + l * TJ, a_tmem + kk * 8, umma_desc_sw128(b_addr + kk * 32, 16, 1024), IDESC,
                         (kt > 0 || kk > 0) ? 1u : 0u);
           }
           mma_commit_mc(&sm.empty[s], CMASK);  // frees stage s in every CTA of the cluster
@@ -224,7 +227,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       int jn = jt, kn = kt + 1;
       if (kn >= nk) { ++jn; kn = 0; }
       if (jn < jt_hi && !(dbg & 2)) load_codes(kn, nxt);
-      uint32_t v[16];
+      uint32_t v[TK / 4];
 #pragma unroll
       for (int c = 0; c < TK / 16; ++c) {
         v[4 * c + 0] = onehot(cur[c].x);
@@ -238,14 +241,21 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       tc_fence_after();
       TP_T0(t2);
       if (!(dbg & 2)) {
-        tmem_st16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS, v);
+        const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS;
+#pragma unroll
+        for (int h16 = 0; h16 < TK / 64; ++h16) {
+          uint32_t w16[16];
+#pragma unroll
+          for (int x = 0; x < 16; ++x) w16[x] = v[16 * h16 + x];
+          tmem_st16(ta + 16 * h16, w16);
+        }
         tmem_st_wait();
       }
       TP_ACC(w_st, t2);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.full[s]);
-      if (jn != jt) nk += 2;  // ktiles_of(jt + 1) = ktiles_of(jt) + TJ / TK
+      if (jn != jt) nk += TJ / TK;  // ktiles_of(jt + 1) = ktiles_of(jt) + TJ / TK
       jt = jn;
       kt = kn;
       if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -453,10 +463,10 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   CUtensorMap tmap;
   cuuint64_t dims[2] = {(cuuint64_t)P, (cuuint64_t)(3 * P)};
   cuuint64_t strides[1] = {(cuuint64_t)P};
-  cuuint32_t box[2] = {TK, SLICE};  // 64 k (bytes) x TJ / CS j: one CTA's slice
+  cuuint32_t box[2] = {TK, SLICE};  // 128 k (bytes) x TJ / CS j: one CTA's slice
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)Hq, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error(GANQ_ERR_CUDA, "tgram: cuTensorMapEncodeTiled failed (%d)", (int)r);
