@@ -10,6 +10,7 @@
 // one owner per step, so the result is deterministic (bitwise identical on every rank).
 // A non-positive pivot records its global index (atomicMin) in *d_status.
 #include <float.h>
+#include <stdlib.h>
 #include <limits.h>
 
 #include "ganq_internal.cuh"
@@ -398,11 +399,9 @@ LookAhead& look_ahead() {
   return la;
 }
 
-ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket, cudaStream_t st) {
-  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     SYRK_SMEM_THIN));
-  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<ST, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     SYRK_SMEM_BULK));
+namespace {
+// The blocked factorisation's launch sequence on `st` (plus the look-ahead side stream).
+ganq_status_t enqueue_cholesky(double* A, int64_t n, int* d_status, int* d_ticket, cudaStream_t st) {
   auto panel = [&](int64_t k0, cudaStream_t ps) -> ganq_status_t {
     const int64_t rest = n - k0 - NB;
     const unsigned grid = rest > 0 ? (unsigned)((rest + PR - 1) / PR) : 1u;
@@ -480,6 +479,78 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket
   }
   zero_upper_kernel<<<1184, 256, 0, st>>>(A, n);
   GANQ_LAUNCH_CHECK("zero_upper_kernel");
+  return GANQ_OK;
+}
+
+// The look-ahead sequence (n < 6144: ~190 launches and ~130 cross-stream event hops) captured
+// once per (A, n, status, ticket, device) into a CUDA graph and replayed on a private stream
+// forked from / joined to the caller's stream; GANQ_CHOL_GRAPH=0 launches it directly.
+struct CholGraph {
+  int device = -1;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  double* A = nullptr;
+  int64_t n = 0;
+  int *status = nullptr, *ticket = nullptr;
+  unsigned long long nlaunch = 0;
+};
+CholGraph& chol_graph() {
+  static thread_local CholGraph g;
+  return g;
+}
+}  // namespace
+
+ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket, cudaStream_t st) {
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SYRK_SMEM_THIN));
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(syrk_trailing_kernel<ST, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SYRK_SMEM_BULK));
+  static const bool use_graph = !getenv("GANQ_CHOL_GRAPH") || atoi(getenv("GANQ_CHOL_GRAPH")) != 0;
+  if (!use_graph || n >= 6144) return enqueue_cholesky(A, n, d_status, d_ticket, st);
+  CholGraph& g = chol_graph();
+  int dev = 0;
+  GANQ_CUDA_TRY(cudaGetDevice(&dev));
+  if (g.device != dev) {
+    g = CholGraph();
+    GANQ_CUDA_TRY(cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking));
+    GANQ_CUDA_TRY(cudaEventCreateWithFlags(&g.ev_in, cudaEventDisableTiming));
+    GANQ_CUDA_TRY(cudaEventCreateWithFlags(&g.ev_out, cudaEventDisableTiming));
+    g.device = dev;
+  }
+  // fork: the private stream waits for the caller's stream (status / ticket initialised there)
+  GANQ_CUDA_TRY(cudaEventRecord(g.ev_in, st));
+  GANQ_CUDA_TRY(cudaStreamWaitEvent(g.cs, g.ev_in, 0));
+  if (!(g.exec && g.A == A && g.n == n && g.status == d_status && g.ticket == d_ticket)) {
+    if (g.exec) {
+      GANQ_CUDA_TRY(cudaGraphExecDestroy(g.exec));
+      g.exec = nullptr;
+    }
+    const unsigned long long c0 = ganq_launch_count();
+    GANQ_CUDA_TRY(cudaStreamBeginCapture(g.cs, cudaStreamCaptureModeThreadLocal));
+    const ganq_status_t s = enqueue_cholesky(A, n, d_status, d_ticket, g.cs);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(g.cs, &graph);
+    if (s) {
+      if (graph) cudaGraphDestroy(graph);
+      return s;
+    }
+    GANQ_CUDA_TRY(e);
+    const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    GANQ_CUDA_TRY(ei);
+    g.nlaunch = ganq_launch_count() - c0;  // kernels recorded (counted once, at capture)
+    g.A = A;
+    g.n = n;
+    g.status = d_status;
+    g.ticket = d_ticket;
+  } else {
+    for (unsigned long long i = 0; i < g.nlaunch; ++i) count_launch();
+  }
+  GANQ_CUDA_TRY(cudaGraphLaunch(g.exec, g.cs));
+  // join: the caller's stream continues after the factorisation
+  GANQ_CUDA_TRY(cudaEventRecord(g.ev_out, g.cs));
+  GANQ_CUDA_TRY(cudaStreamWaitEvent(st, g.ev_out, 0));
   return GANQ_OK;
 }
 
