@@ -11,6 +11,8 @@ Rules (DESIGN.md "Parity"):
   P-4 codebook given identical Q: max_s |dT_is| <= 1e-3 max_s |T_is|       (north_star)
   P-5 objective: relative 1e-4 for identical (Q, T) and free-running K = 10 (north_star)
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -392,3 +394,26 @@ def test_validate_nonfinite_inputs(monkeypatch):
     with pytest.raises(g.GanqError, match="X at \\(10, 5\\)"):
         g.hessian(Xb)
     g.quantize_layer(W, H, 3, 1)  # clean inputs pass
+
+
+def test_cholesky_graph_replay_matches_direct_launches(tmp_path):
+    """n < 6144 replays a captured CUDA graph of the look-ahead sequence; GANQ_CHOL_GRAPH=0
+    launches it directly.  Same kernels, same order per element: bitwise equal factors, also
+    across re-captures for new buffers and repeated replays."""
+    import subprocess
+    import sys
+    _, X = make_case(4, 1000, 3000, seed=12)
+    H = gpu_H(X)
+    La, _ = g.factor(H)
+    Lb, _ = g.factor(H)          # replay (the factor works in the cached workspace)
+    H2 = H.clone()
+    Lc, _ = g.factor(H2)
+    assert torch.equal(La, Lb) and torch.equal(La, Lc)
+    torch.save(H.cpu(), tmp_path / "H.pt")
+    code = ("import torch, paper_2501_12956_b200 as g; "
+            f"H = torch.load(r'{tmp_path / 'H.pt'}').cuda(); L, _ = g.factor(H); "
+            f"torch.save(L.cpu(), r'{tmp_path / 'L.pt'}')")
+    env = dict(os.environ, GANQ_CHOL_GRAPH="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=300)
+    Ld = torch.load(tmp_path / "L.pt")
+    assert torch.equal(La.cpu(), Ld)
