@@ -84,12 +84,13 @@ trhs_kernel(const double* __restrict__ hdiag, const float* __restrict__ WH, cons
   int64_t j0 = 0;
   if ((n & 3) == 0) {
     // lane takes 4 consecutive columns per 128-column step; two steps of loads in flight
-    for (; j0 + 256 <= n; j0 += 256) {
-      uint32_t qv[2];
-      float4 wv[2];
-      double2 h0[2], h1[2];
+    constexpr int TU = 4;  // 128-column steps with loads in flight together
+    for (; j0 + 128 * TU <= n; j0 += 128 * TU) {
+      uint32_t qv[TU];
+      float4 wv[TU];
+      double2 h0[TU], h1[TU];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < TU; ++u) {
         const int64_t j = j0 + 128 * u + 4 * lane;
         qv[u] = *reinterpret_cast<const uint32_t*>(q + j);
         wv[u] = *reinterpret_cast<const float4*>(wh + j);
@@ -97,7 +98,7 @@ trhs_kernel(const double* __restrict__ hdiag, const float* __restrict__ WH, cons
         h1[u] = *reinterpret_cast<const double2*>(hdiag + j + 2);
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < TU; ++u) {
         add2(qv[u] & 255, h0[u].x, wv[u].x, (qv[u] >> 8) & 255, h0[u].y, wv[u].y);
         add2((qv[u] >> 16) & 255, h1[u].x, wv[u].z, qv[u] >> 24, h1[u].y, wv[u].w);
       }
