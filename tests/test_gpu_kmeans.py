@@ -74,3 +74,26 @@ def test_kmeans_rejects_bad_args():
         g.kmeans_codebook(W, 5, 3)
     with pytest.raises(g.GanqError):
         g.kmeans_codebook(W, 2, -1)
+
+
+@pytest.mark.parametrize("nbits", [3, 4])
+def test_quantize_from_kmeans_init_vs_oracle(nbits):
+    """End to end from the k-means T0: the GPU's T0 equals the oracle's bit for bit, so both
+    solvers start from the same codebook; the free-running solve then meets the same bars as
+    the grid start (test_gpu_parity.py::test_free_running_end_to_end, R-13)."""
+    m, n, p, K = 96, 512, 8192, 6
+    W = synthetic.make_weights(m, n, seed=31)
+    X = synthetic.make_activations(p, n, seed=32)
+    H = g.hessian(X.to(DEV))
+    T0o = oracle.kmeans_codebook(W.numpy(), nbits, 25)
+    Qg, Tg = g.quantize_layer(W.to(DEV), H, nbits, K, init="kmeans", precond="none")
+    Hn = H.cpu().numpy()
+    Qo, To = oracle.quantize(W.numpy().astype(np.float64), Hn, nbits, K, policy="none", T0=T0o)
+    fg, prg = g.objective(W.to(DEV), Qg, Tg, H, per_row=True)
+    _, pro = oracle.objective(W.numpy().astype(np.float64), Qo, To, Hn, per_row=True)
+    fo = float(np.sum(pro))
+    prg = prg.cpu().numpy()
+    same = np.all(Qg.cpu().numpy() == Qo, axis=1)
+    assert np.all(np.abs(prg[same] - pro[same]) <= 1e-4 * pro[same])
+    assert same.mean() >= 0.8
+    assert abs(fg - fo) <= 1e-2 * fo, (fg, fo)
