@@ -87,3 +87,35 @@ def test_ganq_star_improves_on_planted_outliers():
     Qd, Td = g.quantize_layer(Wd, H, nbits, 5, precond="none")
     f_star = g.objective(Wd, Qd, Td, H)  # W - (W~_dense + W_sparse) = W_dense - W~_dense
     assert f_star < f_plain
+
+
+def test_ganq_star_deployed_layer_matches_oracle():
+    """The deployed GANQ* layer end to end: split (Algorithm 2) -> quantize W_dense -> pack ->
+    fp16 codebook -> Y = LUT mpGEMM + sparse outliers, against the oracle's fp64 product of the
+    same stored operands (unpacked codes, fp16 codebook, CSR of the oracle's own split).  Bound:
+    the sum of the two kernels' derived bounds (tests/test_gpu_lut.py, this file's header)."""
+    m, n, p, nbits = 48, 512, 3, 4
+    W = synthetic.make_weights(m, n, seed=41)
+    Xc = synthetic.make_activations(2048, n, seed=42).to(DEV)
+    H = g.hessian(Xc)
+    Wd, csr, _ = g.outlier_split(W.to(DEV), 0.005)
+    Q, T = g.quantize_layer(Wd, H, nbits, 3, precond="none")
+    Pk = g.pack_codes(Q, nbits)
+    T16 = g.codebook_f16(T)
+    X16 = (torch.randn((p, n), generator=torch.Generator().manual_seed(43)) * 0.5).to(torch.float16)
+    Y = g.lut_gemm(Pk, T16, X16.to(DEV), n)
+    Y = g.sparse_gemm_add(csr, X16.to(DEV), Y)
+    torch.cuda.synchronize()
+    # oracle side: the stored operands, the oracle's own split of W (bitwise equal, P-split)
+    M, Wd_o, _, _ = oracle.outlier_split(W.numpy(), 0.005)
+    assert np.array_equal(Wd_o, Wd.cpu().numpy())
+    Qo = oracle.unpack(Pk.cpu().numpy(), m, n, nbits)
+    assert np.array_equal(Qo, Q.cpu().numpy())
+    T16o = T16.cpu().numpy().astype(np.float64)
+    Wt = np.take_along_axis(T16o, Qo.astype(np.int64), axis=1)  # W~_dense (stored fp16 levels)
+    Ws = np.where(M, W.numpy().astype(np.float64), 0.0)            # W_sparse
+    x = X16.numpy().astype(np.float64)
+    Yo = x @ (Wt + Ws).T
+    absb = np.abs(x) @ (np.abs(Wt) + np.abs(Ws)).T
+    bound = ((8 * -(-n // 256) + 7) + (-(-n // 32) + 8)) * 2.0 ** -24 * absb + 1e-30
+    assert np.all(np.abs(Y.cpu().numpy().astype(np.float64) - Yo) <= bound)
