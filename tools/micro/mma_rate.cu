@@ -65,7 +65,14 @@ __global__ void __launch_bounds__(128, 1) k_pattern(long long* cyc, int R) {
     const uint32_t sb = smem_u32(b);
     long long t0 = clock64();
     for (int r = 0; r < R; ++r) {
-      if (MODE >= 2) mbar_wait(&ready, 0);
+      if (MODE == 2) mbar_wait(&ready, 0);
+      if (MODE == 3) {  // non-blocking test_wait poll instead of try_wait
+        uint32_t ok = 0;
+        do {
+          asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                       : "=r"(ok) : "r"(smem_u32(&ready)), "r"(0) : "memory");
+        } while (!ok);
+      }
       tc_fence_after();
 #pragma unroll
       for (int l = 0; l < 3; ++l)
@@ -175,7 +182,7 @@ int main() {
   cudaMallocManaged(&cyc, 64);
   run<64, false>(cyc); run<128, false>(cyc); run<256, false>(cyc);
   run<64, true>(cyc); run<128, true>(cyc); run<256, true>(cyc);
-  runp<0>(cyc); runp<1>(cyc); runp<2>(cyc);
+  runp<0>(cyc); runp<1>(cyc); runp<2>(cyc); runp<3>(cyc);
   runc<false, false>(cyc); runc<true, false>(cyc); runc<false, true>(cyc); runc<true, true>(cyc);
   return 0;
 }
