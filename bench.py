@@ -96,12 +96,19 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle timing
-def oracle_layer_time(W_rows: np.ndarray, X_bits: np.ndarray, p: int, m: int, nbits: int, K: int):
-    """Time the fp64 oracle on a bounded sample and extrapolate to the full layer.
+ORACLE_ROWS = 64  # >= the host's cores (OpenMP over rows): every core has rows to solve
 
-    H on X_bits (p_s tokens) scaled by p / p_s; Cholesky of the full n x n (preconditioned
-    sample H); K x (S-step, T-step) on the sampled rows scaled by m / rows (rows are
-    independent, Eq. 2).  Returns dict(seconds, value rows*iter/s, sample description)."""
+
+def oracle_sample(W_rows: np.ndarray, X_bits: np.ndarray, m: int, p: int, nbits: int, K: int):
+    """One bounded sample of the layer on the fp64 oracle, the SAME sample in both arms.
+
+    The sample is the share r/m of the layer that r of its m rows carry (rows are independent
+    given H, Eq. 2): K x (S-step, T-step) on the r rows, H over r/m of the p tokens
+    (X_bits holds p r / m tokens), and the full n x n preconditioned Cholesky, which cannot be
+    split and is charged r/m of its measured time (it is a per-layer cost).  Every piece is timed
+    (wall clock) in this call; value = r K / (t_H + t_ST + (r/m) t_chol) rows*iter/s, i.e. the
+    layer throughput m K / (t_H m/r + t_ST m/r + t_chol) without any per-piece extrapolation
+    beyond that proportional split.  Returns dict(value, wall_s, sample description, parts)."""
     import oracle
     oracle.build()
     ps, n = X_bits.shape
@@ -119,11 +126,21 @@ def oracle_layer_time(W_rows: np.ndarray, X_bits: np.ndarray, p: int, m: int, nb
         Q, _ = oracle.sstep(W_rows, L, T)
         T = oracle.tstep(W_rows, Q, H, 1 << nbits)
     tR = time.perf_counter() - t0
-    total = tH * (p / ps) + tC + tR * (m / r)
-    return dict(seconds=total, value=m * K / total, measured_s=tH + tC + tR,
-                sample=(f"oracle fp64 C (OpenMP): H on {ps} of {p} tokens (x{p / ps:.0f}), full {n}x{n} "
-                        f"Cholesky, K={K} S+T iterations on {r} of {m} rows (x{m / r:.0f}); "
-                        f"extrapolated layer time {total:.1f} s"))
+    charged = tH + tR + tC * r / m
+    return dict(value=r * K / charged, wall_s=tH + tC + tR, layer_s=charged * m / r,
+                parts={"hessian_s": round(tH, 3), "cholesky_s": round(tC, 3), "s_t_steps_s": round(tR, 3)},
+                sample=(f"oracle fp64 C (OpenMP, {cores()} threads): {r} of {m} rows x K={K} S+T iterations, "
+                        f"H over {ps} of {p} tokens (the same {r}/{m} share), full {n}x{n} Cholesky charged "
+                        f"{r}/{m} of its time; layer-equivalent {charged * m / r:.0f} s"))
+
+
+def oracle_inputs(W_cpu: torch.Tensor, X: torch.Tensor, m: int, p: int):
+    """The oracle sample's inputs: ORACLE_ROWS evenly spaced rows of W and the first p r / m
+    tokens of X (bf16 bit patterns)."""
+    r = min(ORACLE_ROWS, m)
+    rows = np.linspace(0, m - 1, r).astype(int)
+    ps = max(1, p * r // m)
+    return W_cpu[rows].numpy().astype(np.float64), synthetic.bf16_bits(X[:ps])
 
 
 def cores():
@@ -132,26 +149,42 @@ def cores():
 
 
 # --------------------------------------------------------------------------- our arm
-def stage_roofline(name, ms, launches, m, n, p, K, peaks, world, nlev=16):
-    """Algorithmic work of a stage per step against the peak of the unit it runs on
-    (DESIGN.md 'Roofline accounting').  Effective peaks of the tensor-core formulations:
-    tf32x3 (sstep, gemm_wh) = tf32 peak / 3 passes, tf32 = bf16 / 2 (nominal ratio);
-    tgram = int8 MAC rate / (3 nlev) MACs per algorithmic addition (nlev one-hot levels x 3 digits:
-    48 at 4 bits, 24 at 3 bits),
-    int8 = 2 x bf16 (nominal ratio).  bf16 is the measured sustained cuBLAS figure."""
-    clk = peaks["sm_mhz"] * 1e6
-    fp64 = 148 * 64 * 2 * clk / 1e12           # fp64 FMA, TFLOP/s
-    tf32x3 = peaks["bf16_sus"] / 2 / 3          # fp32-accurate tensor-core flop/s, TFLOP/s
-    tgram_peak = peaks["bf16_sus"] / (3 * nlev)  # int8 MAC/s (= bf16 flop/s) / (3 nlev) -> additions/s
+def choose_peaks(peaks, ck):
+    """The roofline denominators for this run (B200_PROFILING.md): the BURST cuBLAS bf16 figure and
+    the max SM clock when the timed region ran at max clock with no power cap, else the SUSTAINED
+    figure and the median clock under load."""
+    smax = ck.get("sm_max_mhz") or peaks["sm_mhz"]
+    sm = ck.get("sm_mhz") or smax
+    capped = "sw_power_cap" in (ck.get("reasons") or []) or sm < 0.97 * smax
+    return dict(bf16=peaks["bf16_sus"] if capped else peaks["bf16"], clk_mhz=sm if capped else smax,
+                hbm=peaks["hbm_gbs"], kind="sustained" if capped else "burst", source=peaks["source"])
+
+
+def stage_roofline(name, ms, launches, m, n, p, K, pk, nlev=16):
+    """Algorithmic work of a stage per step against the peak of the unit that bounds it
+    (SURVEY 8(d)).  Tensor peaks are derived from the measured bf16 figure by
+    the nominal ratios of the profiling guide: tf32 = bf16 / 2, and an fp32-accurate tf32x3 product
+    costs 3 tf32 passes.  The T-build (tgram) is bounded by FP32-ALU additions (SURVEY 8(d) G8:
+    148 SM x 128 lanes x clock); its tensor-core one-hot formulation has its own ceiling
+    (int8 = 2 x bf16 MAC/s, 3 digits x 2^N levels MACs per addition), reported beside it.
+    fp64: 148 x 64 FMA lanes x 2 x clock.  Returns None for stages without a bound."""
+    clk = pk["clk_mhz"] * 1e6
+    fp64 = 148 * 64 * 2 * clk / 1e12
+    tf32x3 = pk["bf16"] / 2 / 3
+    alu_adds = 148 * 128 * clk / 1e12            # T additions/s
     s = ms / 1e3
     if s <= 0:
         return None
+    extra = {}
     if name == "hessian":
-        work, unit, bound, peak = n * (n + 1) * p / 1e12, "TFLOP/s", "tensor", peaks["bf16_sus"]
+        work, unit, bound, peak = n * (n + 1) * p / 1e12, "TFLOP/s", "tensor", pk["bf16"]
     elif name == "tgram":
-        work, unit, bound, peak = K * m * n * (n - 1) / 2 / 1e12, "TFLOP/s", "tensor", tgram_peak
+        work, unit, bound, peak = K * m * n * (n - 1) / 2 / 1e12, "TFLOP/s", "alu", alu_adds  # 1 FADD = 1 flop
+        form = 2 * pk["bf16"] / 2 / (3 * nlev)    # int8 MAC/s / (3 nlev MACs per addition)
+        extra = {"formulation": "one-hot int8 tcgen05 (R-14)", "formulation_peak": round(form, 3),
+                 "formulation_frac": round(work / s / form, 4)}
     elif name == "tsolve":
-        work, unit, bound, peak = K * (5.0 * m * n + 4 * 8 * m * nlev * nlev) / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
+        work, unit, bound, peak = K * (5.0 * m * n + 4 * 8 * m * nlev * nlev) / 1e9, "GB/s", "hbm", pk["hbm"]
     elif name == "sstep":
         work, unit, bound, peak = K * m * n * (n - 1) / 1e12, "TFLOP/s", "tensor", tf32x3
     elif name == "gemm_wh":
@@ -159,16 +192,16 @@ def stage_roofline(name, ms, launches, m, n, p, K, peaks, world, nlev=16):
     elif name == "cholesky":
         work, unit, bound, peak = n ** 3 / 3 / 1e12, "TFLOP/s", "alu", fp64
     elif name == "precondition":
-        work, unit, bound, peak = 2 * 8 * n * n / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
+        work, unit, bound, peak = 2 * 8 * n * n / 1e9, "GB/s", "hbm", pk["hbm"]
     elif name == "derive_operands":
-        work, unit, bound, peak = (8 + 8 + 4 + 4) * n * n / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
+        work, unit, bound, peak = (8 + 8 + 4 + 4) * n * n / 1e9, "GB/s", "hbm", pk["hbm"]
     elif name == "init_codebook":
-        work, unit, bound, peak = 4 * m * n / 1e9, "GB/s", "hbm", peaks["hbm_gbs"]
+        work, unit, bound, peak = 4 * m * n / 1e9, "GB/s", "hbm", pk["hbm"]
     else:
         return None
     ach = work / s
     return dict(bound=bound, achieved=round(ach, 3), peak=round(peak, 3), unit=unit, frac=round(ach / peak, 4),
-                ms=round(ms, 4), launches=int(launches))
+                ms=round(ms, 4), ideal_ms=round(1e3 * work / peak, 4), launches=int(launches), **extra)
 
 
 def run_ours(args):
@@ -241,20 +274,28 @@ def run_ours(args):
     ms_step = float(t.item()) / args.steps
     value = m * K / (ms_step / 1e3)
 
+    pk = choose_peaks(peaks, ck)
     stages = {}
     for i in range(nst):
         name = lib.ganq_profile_stage_name(i).decode()
         if ms_arr[i] <= 0:
             continue
         ms_i = ms_arr[i] / args.steps
-        rl = stage_roofline(name, ms_i, ln_arr[i] / args.steps, ml, n, t1 - t0, K, peaks, world, 1 << nbits)
+        rl = stage_roofline(name, ms_i, ln_arr[i] / args.steps, ml, n, t1 - t0, K, pk, 1 << nbits)
         stages[name] = rl if rl else dict(ms=round(ms_i, 4), launches=int(ln_arr[i] / args.steps))
     dominant = max((k for k in stages if "frac" in stages[k]), key=lambda k: stages[k]["ms"])
     roof = {k: stages[dominant][k] for k in ("bound", "achieved", "peak", "unit", "frac")}
     roof["kernel"] = dominant
     roof["share_of_step"] = round(stages[dominant]["ms"] / ms_step, 4)
     roof["traffic"] = load_traffic(dominant)
-    roof["peak_source"] = peaks["source"]
+    roof["peak_source"] = f"{pk['source']} ({pk['kind']}: bf16 {pk['bf16']} TF/s, clock {pk['clk_mhz']} MHz)"
+    for k in ("formulation", "formulation_peak", "formulation_frac"):
+        if k in stages[dominant]:
+            roof[k] = stages[dominant][k]
+    ideal = sum(v.get("ideal_ms", 0.0) for v in stages.values())
+    layer_roof = {"ideal_ms": round(ideal, 4), "measured_ms": round(ms_step, 4), "frac": round(ideal / ms_step, 4),
+                  "definition": "SURVEY 8(d): sum over stages of (algorithmic work / the peak of its bound) "
+                                "divided by the measured layer time"}
 
     # ---- end to end through the public API with host buffers (pinned), H2D + D2H per step
     e2e = None
@@ -321,12 +362,10 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rows = np.linspace(0, m - 1, 8).astype(int)
-        Wr = W[rows].cpu().numpy().astype(np.float64)
-        Xs = synthetic.bf16_bits(X[:256])
-        ob = oracle_layer_time(Wr, Xs, p, m, nbits, K)
+        Wr, Xs = oracle_inputs(W.cpu(), X, m, p)
+        ob = oracle_sample(Wr, Xs, m, p, nbits, K)
         cpu = {"value": round(ob["value"], 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
-               "sample": ob["sample"], "measured_s": round(ob["measured_s"], 2)}
+               "sample": ob["sample"], "wall_s": round(ob["wall_s"], 2), "parts": ob["parts"]}
 
     if rank == 0:
         out = {
@@ -338,7 +377,7 @@ def run_ours(args):
                        "parallelism": f"tokens+rows x{world}" if world > 1 else "single",
                        "l2": "inputs larger than L2 (X = 2.15 GB bf16 streamed every step)"},
             "layer_ms": round(ms_step, 4),
-            "roofline": roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "layer_roofline": layer_roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
             "lut_gemv": lut,
             "clocks": ck,
@@ -442,36 +481,37 @@ def load_traffic(kernel):
 
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The oracle arm: every step is one oracle_sample() of the workload (the same sample as our
+    arm's cpu_baseline), timed on the host cores; rank 0 only."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
     cfg = synthetic.CONFIGS[args.config]
     m, n, p, nbits, K = cfg["m"], cfg["n"], cfg["p"], cfg["nbits"], cfg["iters"]
     W = synthetic.make_weights(m, n, seed=1000)
-    rows = np.linspace(0, m - 1, 2).astype(int)
-    Wr = W[rows].numpy().astype(np.float64)
-    X = synthetic.make_activations(128, n, seed=2000)
-    Xs = synthetic.bf16_bits(X)
+    r = min(ORACLE_ROWS, m)
+    X = synthetic.make_activations(max(1, p * r // m), n, seed=2000)
+    Wr, Xs = oracle_inputs(W, X, m, p)
     for _ in range(args.warmup):
-        oracle_layer_time(Wr, Xs, p, m, nbits, K)
-    secs = []
-    desc = None
+        oracle_sample(Wr, Xs, m, p, nbits, K)
+    vals, walls = [], []
+    ob = None
     for _ in range(args.steps):
-        ob = oracle_layer_time(Wr, Xs, p, m, nbits, K)
-        secs.append(ob["seconds"])
-        desc = ob["sample"]
-    s = sum(secs) / len(secs)
-    value = m * K / s
+        ob = oracle_sample(Wr, Xs, m, p, nbits, K)
+        vals.append(ob["value"])
+        walls.append(ob["wall_s"])
+    value = len(vals) / sum(1.0 / v for v in vals)  # units / total charged time
     out = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": int(os.environ.get("WORLD_SIZE", args.gpus)), "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(s * 1e3, 1), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
+        "ms_per_step": round(1e3 * sum(walls) / len(walls), 1), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "m": m, "n": n, "n_bits": nbits, "tokens": p,
-                   "iters": K},
+                   "iters": K, "sample": ob["sample"]},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores(), "kind": "oracle",
-                         "sample": desc},
+                         "sample": ob["sample"], "parts": ob["parts"]},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "ms_per_step is the measured wall time of one oracle sample (see config.sample)",
     }
     print(json.dumps(out), flush=True)
 

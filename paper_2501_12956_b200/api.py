@@ -7,6 +7,7 @@ device placement.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import torch
@@ -27,7 +28,18 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _need(t, dtype, ndim, name):
+@contextlib.contextmanager
+def _on(dev, stream=None):
+    """Run a call on dev: that device current, and `stream` (default: dev's current stream) the
+    current stream, so outputs and workspace are allocated on the stream the kernels run on."""
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    if s.device != dev:
+        raise ValueError(f"stream is on {s.device}, tensors on {dev}")
+    with torch.cuda.device(dev), torch.cuda.stream(s):
+        yield s
+
+
+def _need(t, dtype, ndim, name, shape=None, device=None):
     if not isinstance(t, torch.Tensor):
         raise TypeError(f"{name} must be a torch.Tensor")
     if not t.is_cuda:
@@ -36,6 +48,10 @@ def _need(t, dtype, ndim, name):
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     if t.dim() != ndim:
         raise ValueError(f"{name} must be {ndim}-D")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}; every tensor of the call must be on {device}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
 
@@ -43,10 +59,14 @@ def _need(t, dtype, ndim, name):
 _ws_cache: dict = {}
 
 
-def _workspace(nbytes: int, device) -> torch.Tensor:
-    key = (str(device),)
+def _workspace(nbytes: int, device, stream) -> torch.Tensor:
+    """Scratch for one call, cached per (device, stream).  It is allocated while `stream` is the
+    current stream, so the caching allocator orders its reuse after the kernels queued on that
+    stream; calls on different streams never share a buffer."""
+    key = (device.index, stream.cuda_stream)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
+        _ws_cache.pop(key, None)  # freed in stream order on `stream`
         buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
         _ws_cache[key] = buf
     return buf
@@ -68,13 +88,15 @@ def hessian(X: torch.Tensor, H: torch.Tensor | None = None, accumulate: bool = F
     """H = X X^T from token-major bf16 activations X (p x n); returns fp64 n x n."""
     _need(X, torch.bfloat16, 2, "X")
     p, n = X.shape
-    if H is None:
-        if accumulate:
-            raise ValueError("accumulate=True needs an existing H")
-        H = torch.empty((n, n), dtype=torch.float64, device=X.device)
-    _need(H, torch.float64, 2, "H")
-    lib = _lib.load()
-    _lib.check(lib.ganq_hessian(_ptr(X), p, n, _ptr(H), int(bool(accumulate)), _stream(stream)))
+    dev = X.device
+    with _on(dev, stream) as s:
+        if H is None:
+            if accumulate:
+                raise ValueError("accumulate=True needs an existing H")
+            H = torch.empty((n, n), dtype=torch.float64, device=dev)
+        _need(H, torch.float64, 2, "H", shape=(n, n), device=dev)
+        lib = _lib.load()
+        _lib.check(lib.ganq_hessian(_ptr(X), p, n, _ptr(H), int(bool(accumulate)), _stream(s)))
     return H
 
 
@@ -115,25 +137,27 @@ def quantize_layer(W: torch.Tensor, H: torch.Tensor, n_bits: int, iters: int = 1
             return quantize_layer(W, H, n_bits, iters, precond="adaptive", lam=lam, tau=tau, T0=T0,
                                   empty_level_rule=empty_level_rule, trace=trace, Q=Q, T=T, stream=stream)
     _need(W, torch.float32, 2, "W")
-    _need(H, torch.float64, 2, "H")
     m, n = W.shape
+    dev = W.device
     nlev = 1 << int(n_bits)
-    if Q is None:
-        Q = torch.empty((m, n), dtype=torch.uint8, device=W.device)
-    if T is None:
-        T = torch.empty((m, nlev), dtype=torch.float32, device=W.device)
-    _need(Q, torch.uint8, 2, "Q")
-    _need(T, torch.float32, 2, "T")
+    _need(H, torch.float64, 2, "H", shape=(n, n), device=dev)
     if T0 is not None:
-        _need(T0, torch.float32, 2, "T0")
-    lib = _lib.load()
-    nbytes = int(lib.ganq_workspace_size(m, n, int(n_bits)))
-    ws = _workspace(nbytes, W.device)
-    tr = (ctypes.c_double * int(iters))() if trace else None
-    o = _opts(precond, lam, tau, T0, empty_level_rule,
-              ctypes.cast(tr, ctypes.POINTER(ctypes.c_double)) if trace else None)
-    _lib.check(lib.ganq_quantize_layer(_ptr(W), m, n, _ptr(H), int(n_bits), int(iters), ctypes.byref(o),
-                                       _ptr(Q), _ptr(T), _ptr(ws), ws.numel(), _stream(stream)))
+        _need(T0, torch.float32, 2, "T0", shape=(m, nlev), device=dev)
+    with _on(dev, stream) as s:
+        if Q is None:
+            Q = torch.empty((m, n), dtype=torch.uint8, device=dev)
+        if T is None:
+            T = torch.empty((m, nlev), dtype=torch.float32, device=dev)
+        _need(Q, torch.uint8, 2, "Q", shape=(m, n), device=dev)
+        _need(T, torch.float32, 2, "T", shape=(m, nlev), device=dev)
+        lib = _lib.load()
+        nbytes = int(lib.ganq_workspace_size(m, n, int(n_bits)))
+        ws = _workspace(nbytes, dev, s)
+        tr = (ctypes.c_double * int(iters))() if trace else None
+        o = _opts(precond, lam, tau, T0, empty_level_rule,
+                  ctypes.cast(tr, ctypes.POINTER(ctypes.c_double)) if trace else None)
+        _lib.check(lib.ganq_quantize_layer(_ptr(W), m, n, _ptr(H), int(n_bits), int(iters), ctypes.byref(o),
+                                           _ptr(Q), _ptr(T), _ptr(ws), ws.numel(), _stream(s)))
     if trace:
         return Q, T, [float(x) for x in tr]
     return Q, T
@@ -169,33 +193,41 @@ def quantize_stacked(Ws, H: torch.Tensor, n_bits: int, iters: int = 10, *, T0=No
 def objective(W, Q, T, H, per_row: bool = False, stream=None):
     """Eq. (1) via Eq. (8) on raw H; returns a Python float (and the fp64 per-row tensor)."""
     _need(W, torch.float32, 2, "W")
-    _need(Q, torch.uint8, 2, "Q")
-    _need(T, torch.float32, 2, "T")
-    _need(H, torch.float64, 2, "H")
     m, n = W.shape
-    n_bits = int(T.shape[1]).bit_length() - 1
-    lib = _lib.load()
-    ws = _workspace(int(lib.ganq_objective_workspace_size(m, n)), W.device)
-    out = ctypes.c_double(0.0)
-    pr = torch.empty(m, dtype=torch.float64, device=W.device) if per_row else None
-    _lib.check(lib.ganq_objective(_ptr(W), _ptr(Q), _ptr(T), _ptr(H), m, n, n_bits, ctypes.byref(out),
-                                  _ptr(pr), _ptr(ws), ws.numel(), _stream(stream)))
+    dev = W.device
+    _need(Q, torch.uint8, 2, "Q", shape=(m, n), device=dev)
+    _need(T, torch.float32, 2, "T", device=dev)
+    nlev = int(T.shape[1])
+    if T.shape[0] != m or nlev < 2 or nlev & (nlev - 1) or nlev > 256:
+        raise ValueError(f"T must be m x 2^N (m = {m}, 1 <= N <= 8), got {tuple(T.shape)}")
+    _need(H, torch.float64, 2, "H", shape=(n, n), device=dev)
+    n_bits = nlev.bit_length() - 1
+    with _on(dev, stream) as s:
+        lib = _lib.load()
+        ws = _workspace(int(lib.ganq_objective_workspace_size(m, n)), dev, s)
+        out = ctypes.c_double(0.0)
+        pr = torch.empty(m, dtype=torch.float64, device=dev) if per_row else None
+        _lib.check(lib.ganq_objective(_ptr(W), _ptr(Q), _ptr(T), _ptr(H), m, n, n_bits, ctypes.byref(out),
+                                      _ptr(pr), _ptr(ws), ws.numel(), _stream(s)))
     return (out.value, pr) if per_row else out.value
 
 
 def tstep(W, Q, H, n_bits: int, empty_level_rule: int = 0, Tprev=None, stream=None):
     """T-update alone (Eq. 6) for given codes Q; returns fp32 m x 2^N."""
     _need(W, torch.float32, 2, "W")
-    _need(Q, torch.uint8, 2, "Q")
-    _need(H, torch.float64, 2, "H")
     m, n = W.shape
-    T = torch.empty((m, 1 << n_bits), dtype=torch.float32, device=W.device)
+    dev = W.device
+    nlev = 1 << int(n_bits)
+    _need(Q, torch.uint8, 2, "Q", shape=(m, n), device=dev)
+    _need(H, torch.float64, 2, "H", shape=(n, n), device=dev)
     if Tprev is not None:
-        _need(Tprev, torch.float32, 2, "Tprev")
-    lib = _lib.load()
-    ws = _workspace(int(lib.ganq_workspace_size(m, n, n_bits)), W.device)
-    _lib.check(lib.ganq_tstep(_ptr(W), _ptr(Q), _ptr(H), m, n, int(n_bits), int(empty_level_rule),
-                              _ptr(Tprev), _ptr(T), _ptr(ws), ws.numel(), _stream(stream)))
+        _need(Tprev, torch.float32, 2, "Tprev", shape=(m, nlev), device=dev)
+    with _on(dev, stream) as s:
+        T = torch.empty((m, nlev), dtype=torch.float32, device=dev)
+        lib = _lib.load()
+        ws = _workspace(int(lib.ganq_workspace_size(m, n, n_bits)), dev, s)
+        _lib.check(lib.ganq_tstep(_ptr(W), _ptr(Q), _ptr(H), m, n, int(n_bits), int(empty_level_rule),
+                                  _ptr(Tprev), _ptr(T), _ptr(ws), ws.numel(), _stream(s)))
     return T
 
 
@@ -203,13 +235,16 @@ def factor(H, precond: str = "adaptive", lam: float = 0.0, tau: float = 1e-7, st
     """(L, delta): Cholesky of the preconditioned H (App. A / Remark 1 / Eq. 9)."""
     _need(H, torch.float64, 2, "H")
     n = H.shape[0]
-    L = torch.empty_like(H)
-    delta = torch.empty(n, dtype=torch.float64, device=H.device)
-    lib = _lib.load()
-    ws = _workspace(int(lib.ganq_workspace_size(1, n, 1)), H.device)
-    o = _opts(precond, lam, tau, None, 0, None)
-    _lib.check(lib.ganq_factor(_ptr(H), n, ctypes.byref(o), _ptr(L), _ptr(delta), _ptr(ws), ws.numel(),
-                               _stream(stream)))
+    dev = H.device
+    _need(H, torch.float64, 2, "H", shape=(n, n))
+    with _on(dev, stream) as s:
+        L = torch.empty_like(H)
+        delta = torch.empty(n, dtype=torch.float64, device=dev)
+        lib = _lib.load()
+        ws = _workspace(int(lib.ganq_workspace_size(1, n, 1)), dev, s)
+        o = _opts(precond, lam, tau, None, 0, None)
+        _lib.check(lib.ganq_factor(_ptr(H), n, ctypes.byref(o), _ptr(L), _ptr(delta), _ptr(ws), ws.numel(),
+                                   _stream(s)))
     return L, delta
 
 
@@ -221,11 +256,12 @@ def pack_codes(Q, n_bits: int, stream=None, check: bool = True):
     N bits of a code) and raises ValueError otherwise."""
     _need(Q, torch.uint8, 2, "Q")
     m, n = Q.shape
-    if check and int(Q.max()) >= (1 << n_bits):
-        raise ValueError(f"codes must be < 2^{n_bits}")
-    lib = _lib.load()
-    P = torch.empty((m, int(lib.ganq_packed_row_bytes(n, int(n_bits)))), dtype=torch.uint8, device=Q.device)
-    _lib.check(lib.ganq_pack_codes(_ptr(Q), m, n, int(n_bits), _ptr(P), _stream(stream)))
+    with _on(Q.device, stream) as s:
+        if check and int(Q.max()) >= (1 << n_bits):
+            raise ValueError(f"codes must be < 2^{n_bits}")
+        lib = _lib.load()
+        P = torch.empty((m, int(lib.ganq_packed_row_bytes(n, int(n_bits)))), dtype=torch.uint8, device=Q.device)
+        _lib.check(lib.ganq_pack_codes(_ptr(Q), m, n, int(n_bits), _ptr(P), _stream(s)))
     return P
 
 
@@ -234,38 +270,48 @@ def kmeans_codebook(W, n_bits: int, iters: int = 25, T=None, stream=None):
     fp32 m x 2^N on W's device."""
     _need(W, torch.float32, 2, "W")
     m, n = W.shape
-    if T is None:
-        T = torch.empty((m, 1 << int(n_bits)), dtype=torch.float32, device=W.device)
-    _need(T, torch.float32, 2, "T")
-    _lib.check(_lib.load().ganq_kmeans_codebook(_ptr(W), m, n, int(n_bits), int(iters), _ptr(T),
-                                                _stream(stream)))
+    with _on(W.device, stream) as s:
+        if T is None:
+            T = torch.empty((m, 1 << int(n_bits)), dtype=torch.float32, device=W.device)
+        _need(T, torch.float32, 2, "T", shape=(m, 1 << int(n_bits)), device=W.device)
+        _lib.check(_lib.load().ganq_kmeans_codebook(_ptr(W), m, n, int(n_bits), int(iters), _ptr(T), _stream(s)))
     return T
+
+
+def _nbits_of(nl: int, name: str) -> int:
+    if nl < 2 or nl & (nl - 1) or nl > 256:
+        raise ValueError(f"{name} must have 2^N columns (1 <= N <= 8), got {nl}")
+    return int(nl).bit_length() - 1
 
 
 def codebook_f16(T, stream=None):
     """fp32 codebook (m x 2^N) -> fp16 (round to nearest even), the stored form of Table 1."""
     _need(T, torch.float32, 2, "T")
     m, nl = T.shape
-    n_bits = int(nl).bit_length() - 1
-    T16 = torch.empty((m, nl), dtype=torch.float16, device=T.device)
-    _lib.check(_lib.load().ganq_codebook_f16(_ptr(T), m, n_bits, _ptr(T16), _stream(stream)))
+    n_bits = _nbits_of(nl, "T")
+    with _on(T.device, stream) as s:
+        T16 = torch.empty((m, nl), dtype=torch.float16, device=T.device)
+        _lib.check(_lib.load().ganq_codebook_f16(_ptr(T), m, n_bits, _ptr(T16), _stream(s)))
     return T16
 
 
 def lut_gemm(P, T16, X, n: int, Y=None, stream=None):
     """Y (p x m, fp32) = X W~^T for W~_ij = T16[i][Q_ij] decoded from the packed codes
     (Fig. 1a right).  X: p x n fp16 (token-major)."""
-    _need(P, torch.uint8, 2, "packed")
-    _need(T16, torch.float16, 2, "T16")
     _need(X, torch.float16, 2, "X")
+    dev = X.device
+    _need(T16, torch.float16, 2, "T16", device=dev)
     m, nl = T16.shape
-    n_bits = int(nl).bit_length() - 1
+    n_bits = _nbits_of(nl, "T16")
     p = X.shape[0]
     if X.shape[1] != n:
         raise ValueError("X must be p x n")
-    if Y is None:
-        Y = torch.empty((p, m), dtype=torch.float32, device=X.device)
-    _lib.check(_lib.load().ganq_lut_gemm(_ptr(P), _ptr(T16), _ptr(X), m, n, p, n_bits, _ptr(Y), _stream(stream)))
+    _need(P, torch.uint8, 2, "packed", shape=(m, (n * n_bits + 7) // 8), device=dev)
+    with _on(dev, stream) as s:
+        if Y is None:
+            Y = torch.empty((p, m), dtype=torch.float32, device=dev)
+        _need(Y, torch.float32, 2, "Y", shape=(p, m), device=dev)
+        _lib.check(_lib.load().ganq_lut_gemm(_ptr(P), _ptr(T16), _ptr(X), m, n, p, n_bits, _ptr(Y), _stream(s)))
     return Y
 
 
@@ -277,18 +323,19 @@ def outlier_split(W, r: float, stream=None):
     _need(W, torch.float32, 2, "W")
     m, n = W.shape
     dev = W.device
-    Wd = torch.empty_like(W)
-    clo = torch.empty(m, dtype=torch.float32, device=dev)
-    chi = torch.empty(m, dtype=torch.float32, device=dev)
-    off = torch.empty(m + 1, dtype=torch.int64, device=dev)
-    nnz = ctypes.c_int64(0)
-    lib = _lib.load()
-    _lib.check(lib.ganq_outlier_split(_ptr(W), m, n, float(r), _ptr(Wd), _ptr(clo), _ptr(chi), _ptr(off),
-                                      ctypes.byref(nnz), _stream(stream)))
-    col = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)[: nnz.value]
-    val = torch.empty(max(nnz.value, 1), dtype=torch.float32, device=dev)[: nnz.value]
-    _lib.check(lib.ganq_outlier_csr(_ptr(W), m, n, _ptr(clo), _ptr(chi), _ptr(off), _ptr(col), _ptr(val),
-                                    _stream(stream)))
+    with _on(dev, stream) as s:
+        Wd = torch.empty_like(W)
+        clo = torch.empty(m, dtype=torch.float32, device=dev)
+        chi = torch.empty(m, dtype=torch.float32, device=dev)
+        off = torch.empty(m + 1, dtype=torch.int64, device=dev)
+        nnz = ctypes.c_int64(0)
+        lib = _lib.load()
+        _lib.check(lib.ganq_outlier_split(_ptr(W), m, n, float(r), _ptr(Wd), _ptr(clo), _ptr(chi), _ptr(off),
+                                          ctypes.byref(nnz), _stream(s)))
+        col = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)[: nnz.value]
+        val = torch.empty(max(nnz.value, 1), dtype=torch.float32, device=dev)[: nnz.value]
+        _lib.check(lib.ganq_outlier_csr(_ptr(W), m, n, _ptr(clo), _ptr(chi), _ptr(off), _ptr(col), _ptr(val),
+                                        _stream(s)))
     return Wd, (off, col, val), (clo, chi)
 
 
@@ -296,9 +343,14 @@ def sparse_gemm_add(csr, X, Y, stream=None):
     """Y (p x m fp32) += X W_sparse^T for the CSR of outlier_split; X: p x n fp16."""
     off, col, val = csr
     _need(X, torch.float16, 2, "X")
-    _need(Y, torch.float32, 2, "Y")
+    dev = X.device
     m = off.numel() - 1
     p, n = X.shape
-    _lib.check(_lib.load().ganq_sparse_gemm_add(_ptr(off), _ptr(col), _ptr(val), m, n, _ptr(X), p, _ptr(Y),
-                                                _stream(stream)))
+    _need(Y, torch.float32, 2, "Y", shape=(p, m), device=dev)
+    for t, nm in ((off, "row_offsets"), (col, "col_idx"), (val, "values")):
+        if not t.is_cuda or t.device != dev or not t.is_contiguous():
+            raise ValueError(f"{nm} must be a contiguous CUDA tensor on {dev}")
+    with _on(dev, stream) as s:
+        _lib.check(_lib.load().ganq_sparse_gemm_add(_ptr(off), _ptr(col), _ptr(val), m, n, _ptr(X), p, _ptr(Y),
+                                                    _stream(s)))
     return Y

@@ -75,7 +75,11 @@ def quantize_layer_distributed(W: torch.Tensor, X_local: torch.Tensor, n_bits: i
         dist.all_reduce(H, op=dist.ReduceOp.SUM, group=group)
     m = W.shape[0]
     r0, r1 = shard_rows(m, world, rank)
-    Q, T = quantize_fn(W[r0:r1].contiguous(), H, n_bits, iters, **opts)
+    if r1 > r0:
+        Q, T = quantize_fn(W[r0:r1].contiguous(), H, n_bits, iters, **opts)
+    else:  # more ranks than rows: this rank owns no rows but still joins the gathers
+        Q = torch.empty((0, n), dtype=torch.uint8, device=W.device)
+        T = torch.empty((0, 1 << int(n_bits)), dtype=torch.float32, device=W.device)
     if gather and world > 1:
         Q = _gather_rows(Q, m, world, group)
         T = _gather_rows(T, m, world, group)

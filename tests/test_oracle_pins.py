@@ -272,6 +272,45 @@ def test_tstep_singular_uses_pinv(oracle):
         np.testing.assert_allclose(T[i], _pins.closed_form_t(W[i], Q[i], H, nlev), rtol=1e-6, atol=1e-9)
 
 
+def test_init_codebook_closed_forms(oracle):
+    """T^0 on rows whose grid is exactly representable (reading R-6; SPEC S:205's example): both
+    endpoints are hit exactly and the step is (max - min) / (2^N - 1) -- a 2^N divisor or an
+    off-by-one level count fails here."""
+    cases = [([0.0, 1.0], 1, [0.0, 1.0]),                                  # SPEC S:205
+             ([-1.0, 2.0, 0.5], 2, [-1.0, 0.0, 1.0, 2.0]),
+             ([3.0, -12.0, 0.0, 1.0], 2, [-12.0, -7.0, -2.0, 3.0]),
+             ([0.0, 15.0, 7.0], 4, list(range(16))),
+             ([2.0, 9.0], 3, [2.0 + s for s in range(8)])]
+    for row, nb, exp in cases:
+        T0 = oracle.init_codebook(np.array([row], np.float32), nb)
+        np.testing.assert_array_equal(T0[0], np.array(exp, np.float32))
+        assert T0[0, -1] == max(row) and T0[0, 0] == min(row)
+
+
+@pytest.mark.parametrize("nlev,rank,seed", [(4, 1, 0), (4, 2, 1), (4, 3, 2), (8, 5, 3), (16, 9, 4), (16, 16, 5)])
+def test_tstep_pinv_ranks(oracle, nlev, rank, seed):
+    """The Moore-Penrose branch over ranks 1 .. 2^N of the normal matrix: H = X X^T with
+    rank(H) = rank (p = rank tokens) and every level used, so G_i = S_i H S_i^T has that rank;
+    T must equal numpy's pseudo-inverse solution b G^+ (SVD based, an independent routine) and
+    lie in the row space of G (min-norm: orthogonal to its null space)."""
+    n = 40
+    rng = np.random.default_rng(seed)
+    Xt = rng.normal(size=(rank, n))
+    H = Xt.T @ Xt
+    W = rng.normal(size=(3, n))
+    Q = np.stack([rng.permutation(np.arange(n) % nlev) for _ in range(3)]).astype(np.uint8)
+    T, G, b = oracle.tstep(W, Q, H, nlev, return_normal=True)
+    for i in range(3):
+        Gi = G[i]
+        exp = b[i] @ np.linalg.pinv(Gi, rcond=1e-10, hermitian=True)
+        scale = np.max(np.abs(exp))
+        np.testing.assert_allclose(T[i], exp, rtol=0, atol=1e-8 * scale)
+        w, V = np.linalg.eigh(Gi)
+        null = V[:, w < 1e-9 * w.max()]
+        assert np.all(np.abs(T[i] @ null) <= 1e-8 * scale)
+        assert np.linalg.matrix_rank(Gi, tol=1e-9 * w.max()) == min(rank, nlev)
+
+
 def test_tstep_monotone(oracle):
     m, n = 6, 32
     W = synthetic.make_weights(m, n, seed=51).numpy().astype(np.float64)
