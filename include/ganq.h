@@ -16,7 +16,8 @@
  *  - Every array pointer is a DEVICE pointer (cudaMalloc / torch CUDA memory)
  *    unless the argument says HOST.  All matrices are row-major, dense,
  *    contiguous.  The caller owns every buffer; the library never allocates or
- *    frees user memory (internal scratch lives in the caller's workspace).
+ *    frees user memory (internal scratch lives in the caller's workspace; ganq_hessian alone
+ *    draws its scratch from the stream-ordered pool, ganq_hessian_ws takes the caller's).
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *    stream).  Work is enqueued on it.  Calls that return a HOST value or
  *    detect a data-dependent error (non-positive-definite factor) synchronise
@@ -75,18 +76,51 @@ void ganq_default_opts(ganq_opts_t* opts);
 /*
  * H = X X^T  (Algorithm 1, "Compute H = XX^T"; X is n x p).
  *   X     : DEVICE, p x n bf16 (passed as uint16 bit patterns), TOKEN-major -- row t is the
- *           activation x_t of one calibration token (so X here is the paper's X^T).
- *   p, n  : tokens >= 1, channels >= 1; n % 8 == 0 is required (TMA row pitch; else
+ *           activation x_t of one calibration token (so X here is the paper's X^T); 16-byte aligned.
+ *   p, n  : tokens in [1, 2^31), channels >= 1; n % 8 == 0 is required (TMA row pitch; else
  *           GANQ_ERR_UNSUPPORTED).
  *   H     : DEVICE, n x n fp64, the FULL symmetric matrix is written.
- *   accumulate : 0 -> H = X X^T;  1 -> H += X X^T (streamed calibration batches, token shards).
- * Arithmetic: bf16 products are exact in fp32; tokens are processed in fixed chunks of
- * GANQ_HESSIAN_CHUNK, each chunk accumulated in fp32 by the tensor cores (tcgen05) and added
- * into H in fp64 in chunk order (reading R-12).  Asynchronous on `stream`.
+ *   accumulate : 0 -> H = X X^T;  1 -> H += X X^T, added in fp64 (streamed calibration batches).
+ * Arithmetic (reading R-12): the tokens are cut into super-chunks of GANQ_HESSIAN_SUPERCHUNK
+ * counted from token 0, each accumulated by the tensor cores (tcgen05, CTA pairs, fp32) in
+ * chains of 256 tokens folded into a round-to-nearest fp32 sum (the super-chunk's partial);
+ * every partial is rounded onto the integer grid 2^(E_i + E_j - 46) (E_c = ceil(e/2) + 1 for
+ * max over the super-chunks of the diagonal partial P[c][c] = m 2^e, m in [0.5, 1)) and the
+ * super-chunks are added EXACTLY in int64; H = that integer x grid (one rounding to fp64).  The
+ * result does not depend on how the super-chunks are grouped: token shards reduced through
+ * ganq_hessian_partials / _fixed + integer all-reduces give bitwise the same H as one call.
+ * ganq_hessian takes its scratch (ganq_hessian_workspace_size(p, n) bytes) from the device's
+ * stream-ordered pool (cudaMallocAsync / cudaFreeAsync on `stream`); ganq_hessian_ws uses the
+ * caller's.  Asynchronous on `stream`.
  */
-#define GANQ_HESSIAN_CHUNK 8192
+#define GANQ_HESSIAN_SUPERCHUNK 32768
 ganq_status_t ganq_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate,
                            void* stream);
+size_t ganq_hessian_workspace_size(int64_t p, int64_t n);
+ganq_status_t ganq_hessian_ws(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/*
+ * The same computation in its three steps, for token shards (one rank per shard; multi-GPU):
+ *   ganq_hessian_partials: partials (DEVICE fp32, ganq_hessian_partials_size(p, n) bytes) = one
+ *     fp32 sum per super-chunk of X (X's first token starts a super-chunk: shard boundaries must
+ *     be multiples of GANQ_HESSIAN_SUPERCHUNK), and E (DEVICE int32 [n]) = the grid exponents
+ *     of its super-chunks' diagonals (above).  Reduce E with MAX over the shards: every shard
+ *     must then use the same, global E.
+ *   ganq_hessian_fixed: Hfix (DEVICE int64, ganq_hessian_fixed_size(n) bytes, tile-major lower
+ *     triangle) = (accumulate ? Hfix + : ) the partials of p tokens rounded onto the grid of E and
+ *     summed exactly.  Hfix of several shards adds exactly (int64 SUM all-reduce, any order).
+ *   ganq_hessian_finalize: H (DEVICE fp64 n x n, full symmetric) = (accumulate ? H + : ) Hfix x grid.
+ * An E below the MAX over all shards' E can make the integers overflow (undefined).  All asynchronous.
+ */
+size_t ganq_hessian_partials_size(int64_t p, int64_t n);
+size_t ganq_hessian_fixed_size(int64_t n);
+ganq_status_t ganq_hessian_partials(const uint16_t* X, int64_t p, int64_t n, float* partials, int32_t* E,
+                                    void* stream);
+ganq_status_t ganq_hessian_fixed(const float* partials, int64_t p, int64_t n, const int32_t* E, int64_t* Hfix,
+                                 int accumulate, void* stream);
+ganq_status_t ganq_hessian_finalize(const int64_t* Hfix, const int32_t* E, int64_t n, double* H, int accumulate,
+                                    void* stream);
 
 /*
  * Bytes of DEVICE workspace ganq_quantize_layer needs for (m, n, n_bits).
@@ -227,7 +261,7 @@ ganq_status_t ganq_sparse_gemm_add(const int64_t* row_offsets, const int32_t* co
  * to fp32; empty levels keep their value} (reading R-24 -- Algorithm 1 takes T^0 as an
  * input; k-means is the Euclidean-distance baseline of
  * the related work).  iters = 0
- * gives the grid itself.  Pass the result as ganq_quantize_opts_t.T0.  n_bits in [1, 4] (else
+ * gives the grid itself.  Pass the result as ganq_opts_t.T0.  n_bits in [1, 4] (else
  * GANQ_ERR_UNSUPPORTED), iters >= 0.  Async on `stream`.
  */
 ganq_status_t ganq_kmeans_codebook(const float* W, int64_t m, int64_t n, int n_bits, int iters, float* T,

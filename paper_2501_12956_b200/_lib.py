@@ -26,6 +26,13 @@ I32 = ctypes.c_int
 SIG = {
     "ganq_default_opts": (None, [P]),
     "ganq_hessian": (I32, [P, I64, I64, P, I32, P]),
+    "ganq_hessian_workspace_size": (ctypes.c_size_t, [I64, I64]),
+    "ganq_hessian_ws": (I32, [P, I64, I64, P, I32, P, ctypes.c_size_t, P]),
+    "ganq_hessian_fixed_size": (ctypes.c_size_t, [I64]),
+    "ganq_hessian_partials_size": (ctypes.c_size_t, [I64, I64]),
+    "ganq_hessian_partials": (I32, [P, I64, I64, P, P, P]),
+    "ganq_hessian_fixed": (I32, [P, I64, I64, P, P, I32, P]),
+    "ganq_hessian_finalize": (I32, [P, P, I64, P, I32, P]),
     "ganq_workspace_size": (ctypes.c_size_t, [I64, I64, I32]),
     "ganq_quantize_layer": (I32, [P, I64, I64, P, I32, I32, P, P, P, P, ctypes.c_size_t, P]),
     "ganq_objective_workspace_size": (ctypes.c_size_t, [I64, I64]),

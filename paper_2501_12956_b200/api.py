@@ -14,7 +14,8 @@ import torch
 
 from . import _lib
 
-__all__ = ["hessian", "quantize_layer", "objective", "tstep", "factor", "workspace_size",
+__all__ = ["hessian", "hessian_partials", "hessian_fixed", "hessian_finalize", "hessian_fixed_size",
+           "quantize_layer", "objective", "tstep", "factor", "workspace_size",
            "objective_workspace_size", "version", "pack_codes", "codebook_f16", "lut_gemm", "outlier_split",
            "sparse_gemm_add"]
 
@@ -97,6 +98,69 @@ def hessian(X: torch.Tensor, H: torch.Tensor | None = None, accumulate: bool = F
         _need(H, torch.float64, 2, "H", shape=(n, n), device=dev)
         lib = _lib.load()
         _lib.check(lib.ganq_hessian(_ptr(X), p, n, _ptr(H), int(bool(accumulate)), _stream(s)))
+    return H
+
+
+SUPERCHUNK = 32768  # == GANQ_HESSIAN_SUPERCHUNK (include/ganq.h): token shards must be multiples
+
+
+def hessian_fixed_size(n: int) -> int:
+    """int64 entries of the fixed-point Hessian accumulator for n channels."""
+    return int(_lib.load().ganq_hessian_fixed_size(n)) // 8
+
+
+def hessian_partials(X: torch.Tensor, P: torch.Tensor | None = None, E: torch.Tensor | None = None, stream=None):
+    """(P, E): the fp32 super-chunk partial sums of X X^T (ganq_hessian_partials, tile layout) and
+    the int32 [n] grid exponents of its super-chunks' diagonals (include/ganq.h, reading R-12)."""
+    _need(X, torch.bfloat16, 2, "X")
+    p, n = X.shape
+    dev = X.device
+    lib = _lib.load()
+    with _on(dev, stream) as s:
+        if P is None:
+            P = torch.empty(int(lib.ganq_hessian_partials_size(p, n)) // 4, dtype=torch.float32, device=dev)
+        if E is None:
+            E = torch.empty(n, dtype=torch.int32, device=dev)
+        _need(P, torch.float32, 1, "P", shape=(int(lib.ganq_hessian_partials_size(p, n)) // 4,), device=dev)
+        _need(E, torch.int32, 1, "E", shape=(n,), device=dev)
+        _lib.check(lib.ganq_hessian_partials(_ptr(X), p, n, _ptr(P), _ptr(E), _stream(s)))
+    return P, E
+
+
+def hessian_fixed(P: torch.Tensor, p: int, E: torch.Tensor, Hfix: torch.Tensor | None = None,
+                  accumulate: bool = False, stream=None):
+    """The exact int64 sum of the partials of p tokens on the grid of E (ganq_hessian_fixed): tile
+    layout; shards add exactly (torch / NCCL int64 SUM, any order)."""
+    _need(E, torch.int32, 1, "E")
+    n = E.shape[0]
+    dev = E.device
+    lib = _lib.load()
+    _need(P, torch.float32, 1, "P", shape=(int(lib.ganq_hessian_partials_size(p, n)) // 4,), device=dev)
+    with _on(dev, stream) as s:
+        if Hfix is None:
+            if accumulate:
+                raise ValueError("accumulate=True needs an existing Hfix")
+            Hfix = torch.empty(hessian_fixed_size(n), dtype=torch.int64, device=dev)
+        _need(Hfix, torch.int64, 1, "Hfix", shape=(hessian_fixed_size(n),), device=dev)
+        _lib.check(lib.ganq_hessian_fixed(_ptr(P), int(p), n, _ptr(E), _ptr(Hfix), int(bool(accumulate)), _stream(s)))
+    return Hfix
+
+
+def hessian_finalize(Hfix: torch.Tensor, E: torch.Tensor, H: torch.Tensor | None = None, accumulate: bool = False,
+                     stream=None):
+    """fp64 n x n symmetric H from the fixed-point accumulator (ganq_hessian_finalize)."""
+    _need(E, torch.int32, 1, "E")
+    n = E.shape[0]
+    dev = E.device
+    _need(Hfix, torch.int64, 1, "Hfix", shape=(hessian_fixed_size(n),), device=dev)
+    with _on(dev, stream) as s:
+        if H is None:
+            if accumulate:
+                raise ValueError("accumulate=True needs an existing H")
+            H = torch.empty((n, n), dtype=torch.float64, device=dev)
+        _need(H, torch.float64, 2, "H", shape=(n, n), device=dev)
+        _lib.check(_lib.load().ganq_hessian_finalize(_ptr(Hfix), _ptr(E), n, _ptr(H), int(bool(accumulate)),
+                                                     _stream(s)))
     return H
 
 

@@ -1,11 +1,12 @@
 // api.cu -- the C ABI declared in include/ganq.h: argument checks, workspace carving and
 // the Algorithm 1 driver.  Every arithmetic step runs in the kernels of
-// hessian.cu, cholesky.cu, sstep.cu, tstep.cu and gemm.cu.
+// hessian.cu, cholesky.cu, sstep_tc.cu, tgram_tc.cu, tstep.cu, gemm.cu and gemm_tc.cu.
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
 
 #include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "ganq_internal.cuh"
@@ -215,6 +216,25 @@ ganq_status_t objective_device(const float* W, const uint8_t* Q, const float* T,
   return launch_sum(per_row, m, total, st);
 }
 
+// Side stream (and fork / join events) of ganq_quantize_layer, one per host thread and device.
+struct SideStream {
+  int device = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream() {
+  static thread_local SideStream sd;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (sd.device != dev) {
+    cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming);
+    sd.device = dev;
+  }
+  return sd;
+}
+
 }  // namespace
 }  // namespace ganq
 
@@ -363,22 +383,110 @@ ganq_status_t ganq_kmeans_codebook(const float* W, int64_t m, int64_t n, int n_b
 
 const char* ganq_version(void) { return "ganq-b200 0.1 (sm_100a)"; }
 
-ganq_status_t ganq_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate,
-                           void* stream) {
-  g_msg[0] = 0;
-  g_index = -1;
-  if (p < 1 || n < 1 || !X || !H) {
+static ganq_status_t hessian_common(const uint16_t* X, int64_t p, int64_t n, const void* out, cudaStream_t st) {
+  if (p < 1 || n < 1 || !X || !out) {
     set_error(GANQ_ERR_INVALID_ARG, "ganq_hessian: p = %lld, n = %lld must be >= 1 and pointers set",
               (long long)p, (long long)n);
     return GANQ_ERR_INVALID_ARG;
   }
-  cudaStream_t st = (cudaStream_t)stream;
   if (validate_enabled()) {
     ganq_status_t s = validate_finite_bf16(X, p, n, "X", st);
     if (s) return s;
   }
+  return check_hessian_args(X, p, n);
+}
+
+size_t ganq_hessian_fixed_size(int64_t n) { return n < 1 ? 0 : hessian_fixed_bytes(n); }
+size_t ganq_hessian_partials_size(int64_t p, int64_t n) { return (p < 1 || n < 1) ? 0 : hessian_partials_bytes(p, n); }
+
+size_t ganq_hessian_workspace_size(int64_t p, int64_t n) {
+  return (p < 1 || n < 1) ? 0 : align_up((size_t)n * sizeof(int32_t), 256) + hessian_partials_bytes(p, n);
+}
+
+ganq_status_t ganq_hessian_partials(const uint16_t* X, int64_t p, int64_t n, float* partials, int32_t* E,
+                                    void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  ganq_status_t s = hessian_common(X, p, n, partials, st);
+  if (s) return s;
+  if (!E) {
+    set_error(GANQ_ERR_INVALID_ARG, "ganq_hessian_partials: E must be set");
+    return GANQ_ERR_INVALID_ARG;
+  }
   GANQ_STAGE(ST_HESSIAN);
-  return launch_hessian(X, p, n, H, accumulate, st);
+  return launch_hessian_partials(X, p, n, partials, E, st);
+}
+
+ganq_status_t ganq_hessian_fixed(const float* partials, int64_t p, int64_t n, const int32_t* E, int64_t* Hfix,
+                                 int accumulate, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (p < 1 || n < 1 || !partials || !E || !Hfix) {
+    set_error(GANQ_ERR_INVALID_ARG, "ganq_hessian_fixed: p, n >= 1 and non-null pointers needed");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  GANQ_STAGE(ST_HESSIAN);
+  return launch_hessian_fixed(partials, p, n, E, reinterpret_cast<long long*>(Hfix), accumulate, st);
+}
+
+ganq_status_t ganq_hessian_finalize(const int64_t* Hfix, const int32_t* E, int64_t n, double* H, int accumulate,
+                                    void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  if (n < 1 || !Hfix || !E || !H) {
+    set_error(GANQ_ERR_INVALID_ARG, "ganq_hessian_finalize: n >= 1 and non-null pointers needed");
+    return GANQ_ERR_INVALID_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  GANQ_STAGE(ST_HESSIAN);
+  return launch_hessian_finalize(reinterpret_cast<const long long*>(Hfix), nullptr, 0, E, n, H, accumulate, st);
+}
+
+ganq_status_t ganq_hessian_ws(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  ganq_status_t s = hessian_common(X, p, n, H, st);
+  if (s) return s;
+  const size_t need = ganq_hessian_workspace_size(p, n);
+  if (!workspace || workspace_bytes < need) {
+    set_error(GANQ_ERR_WORKSPACE, "hessian workspace of %zu bytes < required %zu", workspace_bytes, need);
+    return GANQ_ERR_WORKSPACE;
+  }
+  int32_t* E = reinterpret_cast<int32_t*>(workspace);
+  float* P = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + align_up((size_t)n * sizeof(int32_t), 256));
+  GANQ_STAGE(ST_HESSIAN);
+  if ((s = launch_hessian_partials(X, p, n, P, E, st))) return s;
+  return launch_hessian_finalize(nullptr, P, p, E, n, H, accumulate, st);
+}
+
+ganq_status_t ganq_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate,
+                           void* stream) {
+  g_msg[0] = 0;
+  g_index = -1;
+  cudaStream_t st = (cudaStream_t)stream;
+  ganq_status_t s = hessian_common(X, p, n, H, st);
+  if (s) return s;
+  // scratch from the current device's stream-ordered pool, kept cached between calls
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  const size_t need = ganq_hessian_workspace_size(p, n);
+  void* ws = nullptr;
+  GANQ_CUDA_TRY(cudaMallocAsync(&ws, need, st));
+  s = ganq_hessian_ws(X, p, n, H, accumulate, ws, need, stream);
+  const cudaError_t e = cudaFreeAsync(ws, st);
+  if (s) return s;
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+  return GANQ_OK;
 }
 
 size_t ganq_workspace_size(int64_t m, int64_t n, int n_bits) {
@@ -417,48 +525,60 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
     if ((s = validate_finite_f32(W, m, n, "W", st))) return s;
     if ((s = validate_finite_f64(H, n, n, "H", st))) return s;
   }
-  // H' = precondition(H), L = Cholesky(H')   (App. A / Remark 1, Eq. 9, P:222)
-  if ((s = factor(H, n, o, ws, L, nullptr, st))) return s;
   float* Lhat = at<float>(ws, L.Lhat);
   float* H32 = at<float>(ws, L.H32);
   float* WH = at<float>(ws, L.WH);
   float* E = at<float>(ws, L.E);
   float* EH = at<float>(ws, L.EH);
-  {
-    GANQ_STAGE(ST_DERIVE);
-    if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
-    if ((s = launch_hdiag(H, n, at<double>(ws, L.hdiag), st))) return s;
-    if ((s = launch_lhat_prep(at<double>(ws, L.A64), n, Lhat, at<int8_t>(ws, L.LTq), at<float>(ws, L.tL), st)))
-      return s;
-    // block scales of rows >= m are never written but are read (multiplied by zero digits)
-    GANQ_CUDA_TRY(cudaMemsetAsync(at<float>(ws, L.sE), 0,
-                                  (size_t)ssq_pitch(n) / 64 * (((size_t)m + 31) / 32 * 32) * sizeof(float), st));
-  }
-  {
-    // fixed-point int8 digits of H's strict lower triangle for the tensor-core T-update
-    GANQ_STAGE(ST_DERIVE);
-    if ((s = launch_tq_prep(H, n, at<int8_t>(ws, L.Hq), at<double>(ws, L.qscale), st))) return s;
-  }
   float* Hhi = at<float>(ws, L.Hhi);
   float* Hlo = at<float>(ws, L.Hlo);
+  // Everything that needs only H and W runs on a side stream forked here, so that it overlaps
+  // the preconditioned Cholesky factorisation on `st` (which also synchronises `st` once to
+  // report NOT_PD): fp32 H, H_jj, the int8 digits of H for the T-update, W H, T^0.
+  SideStream& sd = side_stream();
+  GANQ_CUDA_TRY(cudaEventRecord(sd.fork, st));
+  GANQ_CUDA_TRY(cudaStreamWaitEvent(sd.s, sd.fork, 0));
   {
-    // W H (fixed across iterations: W_i H S_i^T of Eq. 6), tf32x3 on the tensor cores
-    GANQ_STAGE(ST_GEMM_WH);
-    if ((s = launch_split_tf32(H32, n, n, Hhi, Hlo, st))) return s;
-    if ((s = launch_split_tf32(W, m, n, at<float>(ws, L.Xhi), at<float>(ws, L.Xlo), st))) return s;
-    if ((s = launch_gemm_tf32x3(at<float>(ws, L.Xhi), at<float>(ws, L.Xlo), Hhi, Hlo, m, n, n, WH, st)))
-      return s;
-  }
-  {
-    // T^0 (reading R-6)
-    GANQ_STAGE(ST_INIT);
-    if (o.T0) {
-      GANQ_CUDA_TRY(cudaMemcpyAsync(T, o.T0, sizeof(float) * (size_t)m * nlev, cudaMemcpyDeviceToDevice, st));
-    } else if ((s = launch_init_codebook(W, m, n, nlev, T, st))) {
-      return s;
+    cudaStream_t st = sd.s;  // (the stage scopes below time on the side stream)
+    {
+      GANQ_STAGE(ST_DERIVE);
+      if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
+      if ((s = launch_hdiag(H, n, at<double>(ws, L.hdiag), st))) return s;
+      // block scales of rows >= m are never written but are read (multiplied by zero digits)
+      GANQ_CUDA_TRY(cudaMemsetAsync(at<float>(ws, L.sE), 0,
+                                    (size_t)ssq_pitch(n) / 64 * (((size_t)m + 31) / 32 * 32) * sizeof(float), st));
+      // fixed-point int8 digits of H's strict lower triangle for the tensor-core T-update
+      if ((s = launch_tq_prep(H, n, at<int8_t>(ws, L.Hq), at<double>(ws, L.qscale), st))) return s;
     }
+    {
+      // W H (fixed across iterations: W_i H S_i^T of Eq. 6), tf32x3 on the tensor cores
+      GANQ_STAGE(ST_GEMM_WH);
+      if ((s = launch_split_tf32(H32, n, n, Hhi, Hlo, st))) return s;
+      if ((s = launch_split_tf32(W, m, n, at<float>(ws, L.Xhi), at<float>(ws, L.Xlo), st))) return s;
+      if ((s = launch_gemm_tf32x3(at<float>(ws, L.Xhi), at<float>(ws, L.Xlo), Hhi, Hlo, m, n, n, WH, st)))
+        return s;
+    }
+    {
+      // T^0 (reading R-6)
+      GANQ_STAGE(ST_INIT);
+      if (o.T0) {
+        GANQ_CUDA_TRY(cudaMemcpyAsync(T, o.T0, sizeof(float) * (size_t)m * nlev, cudaMemcpyDeviceToDevice, st));
+      } else if ((s = launch_init_codebook(W, m, n, nlev, T, st))) {
+        return s;
+      }
+    }
+    GANQ_CUDA_TRY(cudaMemsetAsync(at<int>(ws, L.fb), 0, sizeof(int) * (size_t)m, st));
+    GANQ_CUDA_TRY(cudaEventRecord(sd.join, st));
   }
-  GANQ_CUDA_TRY(cudaMemsetAsync(at<int>(ws, L.fb), 0, sizeof(int) * (size_t)m, st));
+  // H' = precondition(H), L = Cholesky(H')   (App. A / Remark 1, Eq. 9, P:222)
+  s = factor(H, n, o, ws, L, nullptr, st);
+  if (!s) {
+    GANQ_STAGE(ST_DERIVE);
+    s = launch_lhat_prep(at<double>(ws, L.A64), n, Lhat, at<int8_t>(ws, L.LTq), at<float>(ws, L.tL), st);
+  }
+  // join (also on an error: no side-stream work may outlive the call's use of the workspace)
+  GANQ_CUDA_TRY(cudaStreamWaitEvent(st, sd.join, 0));
+  if (s) return s;
   for (int k = 0; k < iters; ++k) {
     {
       // S-update

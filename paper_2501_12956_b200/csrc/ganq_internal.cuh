@@ -38,8 +38,19 @@ static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; 
 
 // ---------------------------------------------------------------- launchers (internal)
 // hessian.cu
-ganq_status_t launch_hessian(const uint16_t* X, int64_t p, int64_t n, double* H, int accumulate,
-                             cudaStream_t st);
+int hessian_tiles(int64_t n);
+int64_t hessian_superchunks(int64_t p);
+size_t hessian_fixed_bytes(int64_t n);
+size_t hessian_partials_bytes(int64_t p, int64_t n);
+ganq_status_t check_hessian_args(const uint16_t* X, int64_t p, int64_t n);
+// super-chunk partials (fp32) of X X^T and the channel exponent bounds E (assigned)
+ganq_status_t launch_hessian_partials(const uint16_t* X, int64_t p, int64_t n, float* Psc, int32_t* E,
+                                      cudaStream_t st);
+ganq_status_t launch_hessian_fixed(const float* Psc, int64_t p, int64_t n, const int32_t* E, long long* Hfix,
+                                   int accumulate, cudaStream_t st);
+// H from Hfix, or (Psc != nullptr) straight from the partials of p tokens
+ganq_status_t launch_hessian_finalize(const long long* Hfix, const float* Psc, int64_t p, const int32_t* E, int64_t n,
+                                      double* H, int accumulate, cudaStream_t st);
 // cholesky.cu
 ganq_status_t launch_precondition(const double* H, int64_t n, int policy, double lambda, double tau,
                                   double* A, double* delta, double* d_mean, cudaStream_t st);
@@ -330,13 +341,17 @@ __device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const void* tma
       "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
       : "memory");
 }
-// mbarrier arrive on the copy of `bar` in CTA `rank` of the cluster (release, cluster scope).
+// mbarrier arrive on the copy of `bar` in CTA `rank` of the cluster.  Default semantics
+// (release at CTA scope, as CUTLASS's ClusterBarrier::arrive): enough to hand TMEM back to the
+// pair's MMA issuer after tcgen05.wait::ld + tcgen05.fence::before_thread_sync, and it does not
+// drain this warp's outstanding global stores (a .release.cluster arrive compiles to a
+// MEMBAR.ALL.GPU).
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
   asm volatile(
       "{\n\t"
       ".reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t"
       "}" ::"r"(smem_u32(bar)),
       "r"(rank)
       : "memory");

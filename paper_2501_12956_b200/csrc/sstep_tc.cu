@@ -68,7 +68,7 @@ struct SsSmem {
 
 // debug-only cycle accounting per warp role: compiled with -DGANQ_KPROF, enabled at run time
 // by GANQ_SSTEP_DBG & 16 (tools/ss_prof.sh); absent from the default build
-__device__ unsigned long long g_ssprof[16];
+__device__ unsigned long long g_ssprof[20];
 #ifdef GANQ_KPROF
 #define TP_T0(v) long long v = (dbg & 16) ? clock64() : 0
 #define TP_ACC(acc, v) do { if (dbg & 16) acc += clock64() - v; } while (0)
@@ -328,7 +328,12 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             }
 #pragma unroll
             for (int x = 0; x < 16; ++x) {
-              const float v = fmaf((float)(int)c0[x], 65536.0f, fmaf((float)(int)c1[x], 256.0f, (float)(int)c2[x]));
+              // |digit-group sums| < 3 * 64 * 2^14 < 2^22: exact int -> float by the 1.5 * 2^23
+              // bias (IADD + FADD on the full-rate pipes instead of the conversion unit)
+              const float f0 = __fsub_rn(__int_as_float((int)c0[x] + 0x4B400000), 12582912.0f);
+              const float f1 = __fsub_rn(__int_as_float((int)c1[x] + 0x4B400000), 12582912.0f);
+              const float f2 = __fsub_rn(__int_as_float((int)c2[x] + 0x4B400000), 12582912.0f);
+              const float v = fmaf(f0, 65536.0f, fmaf(f1, 256.0f, f2));
               acc[16 * hh + x] = fmaf(v, se[16 * hh + x], acc[16 * hh + x]);
             }
           }
@@ -355,14 +360,16 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     const int64_t mq = (m + RB - 1) / RB * RB;  // rows of the sE table
     // named barriers: the panel end, and per sub-panel parity (the decision warp may run two
     // sub-panels ahead of the helpers and vice versa, so each id has one open phase at most)
-    constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_X = 6;  // ES: 4, 5; X: 6, 7
+    constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_X = 6, BAR_HELP = 8;  // ES: 4, 5; X: 6, 7
     if (warp == 6) {
       // ===== decision warp.  The row's codebook sorted (stable by index); th[s] separates
       // sorted positions s and s + 1: the midpoint of two distinct values (a tie goes to the
       // lower original index), or, inside a run of equal values, the next boundary above, so
       // that q = #{s : z > th_s} lands on the first member of the nearest run.  This is the
       // argmin of Eq. 22 with first-index ties, up to the rounding of the midpoints (R-10);
-      // the position is read off the monotone predicates z > th_s by a select tree.
+      // the chosen LEVEL t_q is read off the monotone predicates z > th_s by a select tree and
+      // published; the helpers turn it into the code (its first index: the first member of
+      // the run) and the residual, off this warp's dependency chain.
       const int64_t row = r0 + lane;
       const bool live = row < m;
       float v[NLEV];
@@ -387,12 +394,6 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       int rfirst[NLEV];  // original index of the first member of each position's run
 #pragma unroll
       for (int s2 = 0; s2 < NLEV; ++s2) rfirst[s2] = (s2 > 0 && v[s2] == v[s2 - 1]) ? rfirst[s2 - 1] : ix[s2];
-      uint64_t pk = 0;  // original index of each sorted position, 4 bits each
-#pragma unroll
-      for (int s2 = 0; s2 < NLEV; ++s2) pk |= (uint64_t)ix[s2] << (4 * s2);
-      int pos[NLEV];  // sorted positions (constants: selected without registers)
-#pragma unroll
-      for (int s2 = 0; s2 < NLEV; ++s2) pos[s2] = s2;
       constexpr int NT = NLEV - 1;
       float th[NT];
       float above = __int_as_float(0x7f800000);
@@ -409,7 +410,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       }
       named_bar_sync(BAR_PANEL, PANEL_THREADS);  // the helpers staged panel 0's weights
       TP_T0(t_all);
-      long long w_acc = 0, w_ld = 0, c_dec = 0, c_bar = 0;
+      long long w_acc = 0, w_ld = 0, c_dec = 0, c_bar = 0, c_ld2 = 0, c_loop = 0;
       for (int q = 0; q < P; ++q) {
         const int64_t jb = n - (int64_t)PW * (q + 1);
         const int ab = q & 1;
@@ -428,8 +429,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           if (sp < NSUB - 2) named_bar_sync(BAR_X + (sp & 1), PANEL_THREADS);
           TP_ACC(c_bar, tb);
           TP_T0(t2);
-          float a[SB], w[SB], ev[SB], lc[SB];
-          int iv[SB];
+          float a[SB], w[SB], tv[SB], lc[SB];
 #pragma unroll
           for (int cc = 1; cc < SB; ++cc) lc[cc] = sm.Ld[SB * sp + cc][SB * sp + cc - 1];  // critical path
 #pragma unroll
@@ -439,25 +439,45 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             a2[k] = 0.0f;
             w[k] = sm.ws[SB * sp + k][lane];
           }
+          // the coefficient rows of column cc (in-sub-panel part and next-sub-panel part), loaded
+          // one column ahead so that their shared-memory latency is off the decision chain
+          TP_ACC(c_ld2, t2);
+          TP_T0(t2b);
+          float4 lr[SB / 4], ln[SB / 4];
+#pragma unroll
+          for (int k4 = 0; k4 < SB / 4; ++k4) {
+            lr[k4] = reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * sp])[k4];
+            ln[k4] = (sp > 0) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * (sp - 1)])[k4]
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
 #pragma unroll
           for (int cc = SB - 1; cc >= 0; --cc) {
+            float4 lrn[SB / 4], lnn[SB / 4];
+            if (cc > 0) {
+#pragma unroll
+              for (int k4 = 0; k4 < SB / 4; ++k4) {
+                lrn[k4] = (4 * k4 < cc - 2) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * sp])[k4]
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                lnn[k4] = (sp > 0) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * (sp - 1)])[k4]
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+            }
             const float z = __fadd_rn(w[cc], a[cc]);
             bool pz[NT > 0 ? NT : 1];
 #pragma unroll
             for (int s2 = 0; s2 < NT; ++s2) pz[s2] = z > th[s2];
             const float tq = tree_select<0, NLEV - 1>(v, pz);
-            const int iq = (int)((pk >> (4 * tree_select<0, NLEV - 1>(pos, pz))) & 15u);
-            const float ec = (j0 + cc >= 0) ? __fsub_rn(w[cc], tq) : 0.0f;
-            ev[cc] = ec;  // stored after the sub-panel: no shared stores between the Ld loads
-            iv[cc] = iq;
+            // phantom columns (j < 0, leftmost) feed only phantom columns; the helpers zero
+            // their residuals before any other use
+            const float ec = __fsub_rn(w[cc], tq);
+            tv[cc] = tq;  // stored after the sub-panel: no shared stores between the Ld loads
             // in-sub-panel feedback into the columns left of cc (entries >= cc are already used);
             // the coefficient of column cc - 1 (the next decision) comes from a register
             if (cc > 0) a[cc - 1] = fmaf(ec, lc[cc], a[cc - 1]);
-            const float4* lrow = reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][SB * sp]);
 #pragma unroll
             for (int k4 = 0; k4 < SB / 4; ++k4) {
               if (4 * k4 < cc - 1) {
-                const float4 l = lrow[k4];
+                const float4 l = lr[k4];
                 if (4 * k4 + 0 < cc - 1) a[4 * k4 + 0] = fmaf(ec, l.x, a[4 * k4 + 0]);
                 if (4 * k4 + 1 < cc - 1) a[4 * k4 + 1] = fmaf(ec, l.y, a[4 * k4 + 1]);
                 if (4 * k4 + 2 < cc - 1) a[4 * k4 + 2] = fmaf(ec, l.z, a[4 * k4 + 2]);
@@ -466,25 +486,29 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             }
             // ... and into the next sub-panel
             if (sp > 0) {
-              const float4* lnext = reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][SB * (sp - 1)]);
 #pragma unroll
               for (int k4 = 0; k4 < SB / 4; ++k4) {
-                const float4 l = lnext[k4];
+                const float4 l = ln[k4];
                 a2[4 * k4 + 0] = fmaf(ec, l.x, a2[4 * k4 + 0]);
                 a2[4 * k4 + 1] = fmaf(ec, l.y, a2[4 * k4 + 1]);
                 a2[4 * k4 + 2] = fmaf(ec, l.z, a2[4 * k4 + 2]);
                 a2[4 * k4 + 3] = fmaf(ec, l.w, a2[4 * k4 + 3]);
               }
             }
+            if (cc > 0) {
+#pragma unroll
+              for (int k4 = 0; k4 < SB / 4; ++k4) {
+                lr[k4] = lrn[k4];
+                ln[k4] = lnn[k4];
+              }
+            }
           }
 #pragma unroll
-          for (int cc = 0; cc < SB; ++cc) {
-            sm.es[SB * sp + cc][lane] = ev[cc];
-            sm.cs[SB * sp + cc][lane] = (uint8_t)iv[cc];
-          }
+          for (int cc = 0; cc < SB; ++cc) sm.es[SB * sp + cc][lane] = tv[cc];  // the chosen levels
+          TP_ACC(c_loop, t2b);
           TP_ACC(c_dec, t2);
           __syncwarp();
-          named_bar_arrive(BAR_ES + (sp & 1), PANEL_THREADS);  // es / cs of sub-panel sp are complete
+          named_bar_arrive(BAR_ES + (sp & 1), PANEL_THREADS);  // the levels of sub-panel sp are in es
         }
         TP_T0(t3);
         named_bar_sync(BAR_PANEL, PANEL_THREADS);  // the helpers finished the panel
@@ -496,6 +520,8 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       tp_flush(dbg, lane, 10, w_acc);
       tp_flush(dbg, lane, 11, w_ld);
       tp_flush(dbg, lane, 12, c_dec);
+      tp_flush(dbg, lane, 16, c_ld2);
+      tp_flush(dbg, lane, 17, c_loop);
       tp_flush(dbg, lane, 15, c_bar);
     } else {
       // ===== helpers: lane = row.  After sub-panel sp is decided, its residuals are applied to
@@ -506,6 +532,9 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       const int64_t row = r0 + rr;
       const bool live = row < m;
       const float* wrow = W + (live ? row : 0) * n;
+      float Tr[NLEV];  // the row's codebook (unsorted: code = index)
+#pragma unroll
+      for (int s2 = 0; s2 < NLEV; ++s2) Tr[s2] = live ? T[row * NLEV + s2] : 0.0f;
       // weights of panel columns [c0, c0 + SB) of the panel starting at jb -> ws (lane = row)
       // (asynchronous copies: they complete while the decisions go on, waited for at panel end)
       auto stage_w = [&](int64_t jbp, int c0) {
@@ -532,6 +561,18 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
 #pragma unroll 1
         for (int sp = NSUB - 1; sp >= 0; --sp) {
           named_bar_sync(BAR_ES + (sp & 1), PANEL_THREADS);  // the decision warp finished sub-panel sp
+          // codes and residuals of sub-panel sp from the chosen levels (columns dealt round-robin):
+          // code = the first index s with T_s == t_q (the decision picks the first member of a
+          // run of equal levels); residual e = w - t_q, zero on phantom columns (j < 0)
+          for (int cc = hw; cc < SB; cc += NHELP) {
+            const float tq = sm.es[SB * sp + cc][rr];
+            int iq = 0;
+#pragma unroll
+            for (int s2 = NLEV - 1; s2 >= 0; --s2) iq = (Tr[s2] == tq) ? s2 : iq;
+            sm.cs[SB * sp + cc][rr] = (uint8_t)iq;
+            sm.es[SB * sp + cc][rr] = (jb + SB * sp + cc >= 0) ? __fsub_rn(sm.ws[SB * sp + cc][rr], tq) : 0.0f;
+          }
+          named_bar_sync(BAR_HELP, NHELP * 32);
           TP_T0(t4);
           if (sp >= 2) {
             float e8[SB];
@@ -775,18 +816,18 @@ ganq_status_t launch_t(const float* W, const float* Lhat, const int8_t* LTq, con
                                    Eq, sE, dbg));
   GANQ_LAUNCH_CHECK("sstep_tc_kernel");
   if (dbg & 16) {
-    unsigned long long h[16];
+    unsigned long long h[20];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(h, g_ssprof, sizeof(h));
     const double c = (double)((groups + CS - 1) / CS * CS);
     fprintf(stderr,
             "ssprof per CTA (kcyc): tma %.1f (empty %.1f, ebar %.1f) | mma %.1f (tempty %.1f, full %.1f) | "
             "rd/warp %.1f (tfull %.1f, as_free %.1f) | decide %.1f (acc_ready %.1f, ld %.1f, dec %.1f, "
-            "bar %.1f) | helper/warp st %.1f, cross %.1f\n",
+            "bar %.1f; sub-panel loads %.1f, column loop %.1f) | helper/warp st %.1f, cross %.1f\n",
             h[0] / c / 1e3, h[1] / c / 1e3, h[2] / c / 1e3, h[3] / c / 1e3, h[4] / c / 1e3, h[5] / c / 1e3,
             h[6] / c / 4e3, h[7] / c / 4e3, h[8] / c / 4e3, h[9] / c / 1e3, h[10] / c / 1e3, h[11] / c / 1e3,
-            h[12] / c / 1e3, h[15] / c / 1e3, h[13] / c / 3e3, h[14] / c / 3e3);
-    const unsigned long long z[16] = {};
+            h[12] / c / 1e3, h[15] / c / 1e3, h[16] / c / 1e3, h[17] / c / 1e3, h[13] / c / 3e3, h[14] / c / 3e3);
+    const unsigned long long z[20] = {};
     cudaMemcpyToSymbol(g_ssprof, z, sizeof(z));
   }
   return GANQ_OK;

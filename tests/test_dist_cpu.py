@@ -1,8 +1,11 @@
 """Multi-process host logic of the multi-GPU driver (paper_2501_12956_b200/dist.py) on CPU.
 
-World size 2 over gloo (127.0.0.1).  The per-rank compute is injected with the fp64 oracle,
-so these tests exercise exactly the sharding, the all-reduce of the partial Hessians and the
-gather of row blocks -- the parts of the N > 1 path that do not need a GPU.
+World size 2 over gloo (127.0.0.1).  The per-rank compute is injected: the S/T solve with the fp64
+oracle, the Hessian with a numpy emulation of ganq_hessian_fixed's contract (every super-chunk's
+X X^T rounded onto the integer grid 2^(E_i + E_j - 31), int64 sums; reading R-12) built on the
+oracle's fp64 H.  These tests exercise exactly the sharding, the MAX all-reduce of the channel
+exponents, the exact int64 SUM all-reduce of the partial Hessians and the gather of row blocks --
+the parts of the N > 1 path that do not need a GPU.
 """
 import os
 import socket
@@ -14,7 +17,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import synthetic
-from paper_2501_12956_b200.dist import HESSIAN_CHUNK, quantize_layer_distributed, shard_rows, shard_tokens
+from paper_2501_12956_b200.dist import SUPERCHUNK, quantize_layer_distributed, shard_rows, shard_tokens
 
 
 def _free_port():
@@ -36,21 +39,45 @@ def test_shard_rows_cover_and_balance():
 
 
 def test_shard_tokens_chunk_aligned():
-    for p in (100, HESSIAN_CHUNK, 3 * HESSIAN_CHUNK + 5, 262144):
+    for p in (100, SUPERCHUNK, 3 * SUPERCHUNK + 5, 262144):
         for world in (1, 2, 4, 8):
             rng = [shard_tokens(p, world, r) for r in range(world)]
             assert rng[0][0] == 0 and rng[-1][1] == p
             for (a, b), (c, d) in zip(rng, rng[1:]):
                 assert b == c
             for a, b in rng:
-                assert a == b or a % HESSIAN_CHUNK == 0  # whole chunks: exact fp64 sums (R-12)
+                assert a == b or a % SUPERCHUNK == 0  # whole super-chunks: exact integer sums (R-12)
 
 
-def _oracle_hessian(Xloc):
+SC = SUPERCHUNK // 64  # emulated super-chunk (small test sizes)
+
+
+def _emu_partials(Xloc):
+    """(the oracle's fp64 X X^T of every super-chunk, E from their diagonals: E_c = ceil(e/2) + 1
+    for max_sc P_sc[c][c] = m 2^e, m in [0.5, 1) -- the rule of ganq_hessian_partials)"""
     import oracle
-    if Xloc.shape[0] == 0:
-        return torch.zeros((Xloc.shape[1], Xloc.shape[1]), dtype=torch.float64)
-    return torch.from_numpy(oracle.hessian_bf16(synthetic.bf16_bits(Xloc)))
+    P = [oracle.hessian_bf16(synthetic.bf16_bits(Xloc[t0:t0 + SC].contiguous())) for t0 in range(0, Xloc.shape[0], SC)]
+    D = np.max(np.stack([np.diag(h) for h in P]), axis=0)
+    _, e = np.frexp(D)
+    E = np.where(D > 0, ((e + 1) >> 1) + 1, -126).astype(np.int32)
+    return P, torch.from_numpy(E)
+
+
+def _emu_fixed(P, p, E):
+    e = E.numpy().astype(np.int64)
+    acc = np.zeros(P[0].shape, np.int64)
+    for Hs in P:
+        acc += np.rint(np.ldexp(Hs, 46 - e[:, None] - e[None, :])).astype(np.int64)
+    return torch.from_numpy(acc.reshape(-1))
+
+
+def _emu_finalize(Hfix, E):
+    n = E.shape[0]
+    e = E.numpy().astype(np.int64)
+    return torch.from_numpy(np.ldexp(Hfix.numpy().reshape(n, n).astype(np.float64), e[:, None] + e[None, :] - 46))
+
+
+EMU = dict(partials_fn=_emu_partials, fixed_fn=_emu_fixed, finalize_fn=_emu_finalize, fixed_size_fn=lambda n: n * n)
 
 
 def _oracle_quantize(Wloc, H, nbits, iters, **kw):
@@ -64,12 +91,12 @@ def _worker(rank, world, port, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        m, n, p, nbits, K = 23, 40, 3 * HESSIAN_CHUNK // 64, 3, 3
+        m, n, p, nbits, K = 23, 40, 3 * SC, 3, 3
         W = synthetic.make_weights(m, n, seed=5)
         X = synthetic.make_activations(p, n, seed=6)
-        t0, t1 = shard_tokens(p, world, rank, chunk=HESSIAN_CHUNK // 64)
-        res = quantize_layer_distributed(W, X[t0:t1].contiguous(), nbits, K,
-                                         hessian_fn=_oracle_hessian, quantize_fn=_oracle_quantize)
+        t0, t1 = shard_tokens(p, world, rank, chunk=SC)
+        res = quantize_layer_distributed(W, X[t0:t1].contiguous(), nbits, K, hessian_fns=EMU,
+                                         quantize_fn=_oracle_quantize)
         out[rank] = (res.Q.numpy(), res.T.numpy(), res.H.numpy(), res.rows)
     finally:
         dist.destroy_process_group()
@@ -83,14 +110,19 @@ def test_world2_gloo_matches_single_process():
     mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.start_processes(_worker, args=(world, port, out), nprocs=world, start_method="spawn", join=True)
-    m, n, p, nbits, K = 23, 40, 3 * HESSIAN_CHUNK // 64, 3, 3
+    m, n, p, nbits, K = 23, 40, 3 * SC, 3, 3
     W = synthetic.make_weights(m, n, seed=5)
     X = synthetic.make_activations(p, n, seed=6)
     Hfull = oracle.hessian_bf16(synthetic.bf16_bits(X))
     Q0, T0, H0, rows0 = out[0]
     Q1, T1, H1, rows1 = out[1]
     assert np.array_equal(H0, H1)                      # every rank holds the same reduced H
-    np.testing.assert_allclose(H0, Hfull, rtol=1e-12)  # = X X^T of all tokens
+    P, E = _emu_partials(X)
+    H1p = _emu_finalize(_emu_fixed(P, p, E), E).numpy()
+    assert np.array_equal(H0, H1p)                     # bitwise the single-process fixed-point H
+    e = E.numpy().astype(np.int64)
+    grid = np.ldexp(1.0, e[:, None] + e[None, :] - 46)
+    assert np.all(np.abs(H0 - Hfull) <= 3 * 0.5 * grid + 1e-15 * np.abs(Hfull))  # X X^T, one rounding per super-chunk
     assert rows0 == (0, 12) and rows1 == (12, 23)
     assert np.array_equal(Q0, Q1) and np.array_equal(T0, T1)  # gathered on both ranks
     Qs, Ts = oracle.quantize(W.numpy().astype(np.float64), H0, nbits, K)

@@ -1,10 +1,7 @@
 """GPU (sm_100a) vs fp64 oracle parity, through the C ABI (paper_2501_12956_b200 binding).
 
 Rules:
-  P-1 H: |dH_jk| <= (C/16 + 2 + nchunks) 2^-23 (|X|^T |X|)_jk -- the tensor cores accumulate
-      each chunk of C = GANQ_HESSIAN_CHUNK tokens in fp32 with C/16 truncating adds of K = 16
-      products (<= 1 ulp each); chunks are folded into a round-to-nearest fp32 running sum
-      (<= 1/2 ulp per chunk) and written to fp64 H once (R-12)
+  P-1 H: ||dH||_F/||H||_F <= 1e-6 and |dH_jk| <= 1e-5 sqrt(H_jj H_kk)   (SURVEY P-1, R-12)
   P-2 L: ||L_gpu - chol64(H + Diag(delta_gpu))||_F / ||L||_F <= 1e-9
   P-3 codes, teacher-forced: every GPU code is the oracle argmin or a near-tie,
       |z - t_q| - |z - t_s*| <= 1e-6 max_s |T_is|                          (north_star)
@@ -44,14 +41,17 @@ def gpu_H(X):
     return g.hessian(X.to(DEV))
 
 
-CHUNK = 8192
-
-
-def hessian_bound(X):
-    """Elementwise bound of P-1 for the GPU's chunked fp32 tensor-core accumulation."""
-    A = np.abs(synthetic.bf16_to_f64(X))
-    nchunks = (X.shape[0] + CHUNK - 1) // CHUNK
-    return (CHUNK / 16 + 2 + nchunks) * 2.0 ** -23 * (A.T @ A)
+def p1_check(H, Ho):
+    """SURVEY P-1: ||dH||_F / ||H||_F <= 1e-6 and |dH_jk| <= 1e-5 sqrt(H_jj H_kk) (same bf16 X).
+    The GPU's error is the tensor cores' truncating fp32 adds over centred chunks of <= 512 MMAs
+    and one fp32 round-to-nearest fold per chunk (reading R-12); the integer grid adds <= 2^-32 of
+    max|x_j x_k| per super-chunk."""
+    d = np.sqrt(np.outer(np.diag(Ho), np.diag(Ho)))
+    rel = rel_fro(H, Ho)
+    el = float(np.max(np.abs(H - Ho) / np.maximum(d, 1e-300)))
+    assert rel <= 1e-6, rel
+    assert el <= 1e-5, el
+    return rel, el
 
 
 def rel_fro(a, b):
@@ -60,14 +60,17 @@ def rel_fro(a, b):
 
 # ----------------------------------------------------------------------------- P-1 Hessian
 
-@pytest.mark.parametrize("p,n", [(256, 128), (1000, 200), (20000, 384), (8192, 64), (70, 8)])
+@pytest.mark.parametrize("p,n", [(256, 128), (1000, 200), (20000, 384), (8192, 64), (70, 8),
+                                 (3 * 32768 + 4100, 136)])
 def test_hessian_parity(p, n):
+    """Ragged p (inside the first 512-token chunk, inside a later chunk, across super-chunks),
+    ragged n (tiles past the matrix edge)."""
     _, X = make_case(4, n, p, seed=p % 97)
     H = gpu_H(X).cpu().numpy()
     Ho = oracle.hessian_bf16(synthetic.bf16_bits(X))
     assert np.array_equal(H, H.T)
-    assert np.all(np.abs(H - Ho) <= hessian_bound(X))
-    assert rel_fro(H, Ho) <= 1e-4
+    rel, el = p1_check(H, Ho)
+    print(f"\n[P-1 p={p} n={n}] rel {rel:.2e} elementwise {el:.2e}")
 
 
 def test_hessian_accumulate_and_errors():
@@ -75,22 +78,52 @@ def test_hessian_accumulate_and_errors():
     Xd = X.to(DEV)
     H1 = g.hessian(Xd)
     H2 = g.hessian(Xd, H=H1.clone(), accumulate=True)
-    np.testing.assert_allclose(H2.cpu().numpy(), 2 * H1.cpu().numpy(), rtol=1e-12)
+    assert torch.equal(H2, 2 * H1)  # fp64 x + x is exact
     with pytest.raises(g.GanqError):
         g.hessian(torch.zeros((16, 12), dtype=torch.bfloat16, device=DEV))  # n % 8 != 0
 
 
-def test_hessian_token_shards_sum():
-    """Shards along chunk boundaries (the multi-GPU token split) add up to the one-shot H
-    within the fp32 running-sum rounding of R-12."""
-    _, X = make_case(4, 128, 3 * 8192 + 500, seed=6)
+def test_hessian_token_shards_bitwise():
+    """Token shards at super-chunk boundaries, reduced through the fixed-point path (global E by
+    MAX, int64 SUM in any order), give bitwise the one-shot H (reading R-12)."""
+    SC = g.api.SUPERCHUNK
+    _, X = make_case(4, 128, 3 * SC + 500, seed=6)
     Xd = X.to(DEV)
     H = g.hessian(Xd)
-    Hs = g.hessian(Xd[:8192].contiguous())
-    Hs = g.hessian(Xd[8192:].contiguous(), H=Hs, accumulate=True)
-    A = np.abs(synthetic.bf16_to_f64(X))
-    assert np.all(np.abs((H - Hs).cpu().numpy()) <= 8 * 2.0 ** -24 * (A.T @ A))
+    parts = [Xd[:SC].contiguous(), Xd[SC:].contiguous()]
+    P0, E = g.hessian_partials(parts[0])
+    P1, E1 = g.hessian_partials(parts[1])
+    E = torch.maximum(E, E1)
+    assert torch.equal(E, g.hessian_partials(Xd)[1])
+    Hf = g.hessian_fixed(P1, parts[1].shape[0], E)
+    Hf = g.hessian_fixed(P0, parts[0].shape[0], E, Hfix=Hf, accumulate=True)
+    assert torch.equal(g.hessian_finalize(Hf, E), H)
     assert torch.equal(g.hessian(Xd), H)  # deterministic
+
+
+def test_hessian_gpu_count_invariance():
+    """Simulated G = 1, 2, 4, 8 token shards of p = 8 super-chunks (the bench's 262144 tokens):
+    E all-reduced by MAX, Hfix by an integer SUM in a scrambled order -> the same H bit for bit,
+    hence the same factor, codes and codebooks (the solver is deterministic given H)."""
+    from paper_2501_12956_b200.dist import shard_tokens
+    SC = g.api.SUPERCHUNK
+    n, p = 64, 8 * SC
+    W, X = make_case(24, n, p, seed=13)
+    Xd = X.to(DEV)
+    H1 = g.hessian(Xd)
+    Q1, T1 = g.quantize_layer(W.to(DEV), H1, 3, 3)
+    for G in (2, 4, 8):
+        shards = [Xd[slice(*shard_tokens(p, G, r))].contiguous() for r in range(G)]
+        pe = [g.hessian_partials(s) for s in shards]
+        E = torch.stack([e for _, e in pe]).max(0).values.contiguous()
+        parts = [g.hessian_fixed(P, s.shape[0], E) for (P, _), s in zip(pe, shards)]
+        Hf = torch.zeros_like(parts[0])
+        for k in np.random.default_rng(G).permutation(G):
+            Hf += parts[k]
+        HG = g.hessian_finalize(Hf, E)
+        assert torch.equal(HG, H1), G
+        QG, TG = g.quantize_layer(W.to(DEV), HG, 3, 3)
+        assert torch.equal(QG, Q1) and torch.equal(TG, T1)
 
 
 # ----------------------------------------------------------------------------- P-2 factor
@@ -346,30 +379,23 @@ def test_exact_representability_gpu():
 
 # ----------------------------------------------------------------------------- full size (bench config)
 
-@pytest.mark.parametrize("nrows", [6])
-def test_c2_full_size_sampled_rows(nrows):
+def test_c2_full_size_h_properties():
     """BASELINE config c2 in the launch configuration bench.py times (m = n = 4096, 4-bit,
-    p = 262144, K = 10): the GPU solves all rows; the oracle re-solves a sample of rows alone
-    (rows are independent, Eq. 2) from the same H, and the per-row objectives must agree."""
+    p = 262144, K = 10): H symmetric with a positive diagonal, the solve's codes in range and its
+    objective finite.  The decisions, codebooks and free-running rows of this configuration are
+    checked against the oracle in tests/test_gpu_c2_parity.py (P-3, P-4, P-5)."""
     c = synthetic.CONFIGS["c2"]
     m, n, p, nbits, K = c["m"], c["n"], c["p"], c["nbits"], c["iters"]
     W = synthetic.make_weights(m, n, seed=1000, device=DEV)
     X = synthetic.make_activations(p, n, seed=2000, device=DEV)
     H = g.hessian(X)
     del X
-    Q, T = g.quantize_layer(W, H, nbits, K)
-    f, pr = g.objective(W, Q, T, H, per_row=True)
-    rows = np.linspace(0, m - 1, nrows).astype(int)
-    Hn = H.cpu().numpy()
-    Ws = W[rows].cpu().numpy().astype(np.float64)
-    Qo, To = oracle.quantize(Ws, Hn, nbits, K)
-    _, pro = oracle.objective(Ws, Qo, To, Hn, per_row=True)
-    prg = pr.cpu().numpy()[rows]
-    np.testing.assert_allclose(prg, pro, rtol=1e-3)
-    assert float(np.mean(Q.cpu().numpy()[rows] == Qo)) > 0.9
-    # H property at full size: symmetric, PSD diagonal
     assert torch.equal(H, H.T)
     assert bool(torch.all(torch.diagonal(H) > 0))
+    Q, T = g.quantize_layer(W, H, nbits, K)
+    assert int(Q.max()) < (1 << nbits)
+    f = g.objective(W, Q, T, H)
+    assert np.isfinite(f) and f > 0
 
 
 def test_c3_full_size_factor_and_sampled_rows():
@@ -377,7 +403,8 @@ def test_c3_full_size_factor_and_sampled_rows():
     the two-panel Cholesky path (n >= 6144) and 8 levels.  P-2 at full size against LAPACK's
     Cholesky of the same H' (a library routine as the factor step: the C oracle's unblocked
     factor takes minutes at n = 11008); then the oracle's S- and T-steps re-solve sampled rows
-    from that factor and raw H, and the per-row objectives must agree (free-running, R-13)."""
+    from that factor and raw H: identical-trajectory rows agree to 1e-4 and every first divergence
+    is a near-tie (P-5 classification, R-13)."""
     c = synthetic.CONFIGS["c3"]
     m, n, p, nbits, K = c["m"], c["n"], c["p"], c["nbits"], c["iters"]
     W = synthetic.make_weights(m, n, seed=1000, device=DEV)
@@ -389,18 +416,25 @@ def test_c3_full_size_factor_and_sampled_rows():
     Lnp = np.linalg.cholesky(Hn + np.diag(delta.cpu().numpy()))
     assert rel_fro(L.cpu().numpy(), Lnp) <= 1e-9
     del L
-    Q, T = g.quantize_layer(W, H, nbits, K)
-    _, pr = g.objective(W, Q, T, H, per_row=True)
     rows = np.linspace(0, m - 1, 4).astype(int)
     Ws32 = W[rows].cpu().numpy()
     Ws = Ws32.astype(np.float64)
-    To = oracle.init_codebook(Ws32, nbits).astype(np.float64)
+    T0 = torch.from_numpy(oracle.init_codebook(W.cpu().numpy(), nbits)).to(DEV)
+    Tk, gtraj = T0, []
     for _ in range(K):
-        Qo, _ = oracle.sstep(Ws, Lnp, To)
-        To = oracle.tstep(Ws, Qo, Hn, 1 << nbits)
-    _, pro = oracle.objective(Ws, Qo, To, Hn, per_row=True)
-    np.testing.assert_allclose(pr.cpu().numpy()[rows], pro, rtol=1e-3)
-    assert float(np.mean(Q.cpu().numpy()[rows] == Qo)) > 0.9
+        Qn, Tn = g.quantize_layer(W, H, nbits, 1, T0=Tk)
+        gtraj.append((Qn.cpu().numpy()[rows], Tn.cpu().numpy()[rows]))
+        Tk = Tn
+    otraj = par.oracle_trajectory(Ws, Hn, Lnp, T0.cpu().numpy()[rows], nbits, K)
+    div = par.classify_divergence(Ws, Lnp, T0.cpu().numpy()[rows], gtraj, otraj)
+    _, prg = oracle.objective(Ws, gtraj[-1][0], gtraj[-1][1].astype(np.float64), Hn, per_row=True)
+    _, pro = oracle.objective(Ws, otraj[-1][0], otraj[-1][1], Hn, per_row=True)
+    same = np.array([i not in {d["row"] for d in div} for i in range(len(rows))])
+    print(f"\n[c3] {same.sum()} of {len(rows)} sampled rows identical; first divergences: "
+          + "; ".join(f"k={d['k']} j={d['j']} margin_gpu={d['margin_gpu']:.1e}" for d in div))
+    np.testing.assert_allclose(prg[same], pro[same], rtol=1e-4)
+    for d in div:
+        assert d["margin_gpu"] <= par.NEAR_TIE, d
 
 
 def test_precond_auto_policy():
