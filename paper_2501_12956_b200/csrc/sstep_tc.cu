@@ -48,8 +48,9 @@ constexpr uint16_t CMASK = (1u << CS) - 1u;
 constexpr int A_TILE = PW * UB;     // 8 KB: one digit of LhatT (128 panel columns x 64 u)
 constexpr int B_TILE = RB * UB;     // 2 KB: one digit of E (32 rows x 64 u)
 constexpr int STAGE_BYTES = 3 * A_TILE + 3 * B_TILE;  // 30 KB
-constexpr int NHELP = 3;        // in-panel helper warps
-constexpr int THREADS = 32 * (7 + NHELP);  // TMA, MMA, 4 readers, decisions, helpers
+constexpr int NHELP = 5;        // in-panel helper warps (6 .. 10)
+constexpr int DECIDE_WARP = 6 + NHELP;     // the highest warp id: first pick of its scheduler
+constexpr int THREADS = 32 * (7 + NHELP);  // TMA, MMA, 4 readers, helpers, decisions
 constexpr int PANEL_THREADS = 32 * (1 + NHELP);
 // digit a of LhatT times the E digits b = 0 .. 2 - a: N = 32 (3 - a)
 __host__ __device__ constexpr uint32_t idesc_digit(int a) { return umma_idesc_s8(PW, RB * (3 - a)); }
@@ -361,7 +362,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     // named barriers: the panel end, and per sub-panel parity (the decision warp may run two
     // sub-panels ahead of the helpers and vice versa, so each id has one open phase at most)
     constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_X = 6, BAR_HELP = 8;  // ES: 4, 5; X: 6, 7
-    if (warp == 6) {
+    if (warp == DECIDE_WARP) {
       // ===== decision warp.  The row's codebook sorted (stable by index); th[s] separates
       // sorted positions s and s + 1: the midpoint of two distinct values (a tie goes to the
       // lower original index), or, inside a run of equal values, the next boundary above, so
@@ -527,7 +528,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       // ===== helpers: lane = row.  After sub-panel sp is decided, its residuals are applied to
       // every column of sub-panels <= sp - 2 (4-column chunks dealt round-robin to the warps);
       // codes leave in 32-column groups, residual digits in 64-column halves.
-      const int hw = warp - 7;
+      const int hw = warp - 6;
       const int rr = lane;
       const int64_t row = r0 + rr;
       const bool live = row < m;
@@ -579,8 +580,18 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
 #pragma unroll
             for (int cc = 0; cc < SB; ++cc) e8[cc] = sm.es[SB * sp + cc][rr];
             const int nch = SB * (sp - 1) / 4;  // 4-column chunks of the columns [0, SB (sp - 1))
+            // chunks in descending order: the two of sub-panel sp - 2 (needed next by the decision
+            // warp) first, then the barrier arrive, then the rest (needed two or more sub-panels
+            // later; a helper handles the same chunks at every step, so their order is kept)
+            const int top = nch - 1 - ((nch - 1 - hw) % NHELP + NHELP) % NHELP;  // largest c4 = hw (mod NHELP)
+            bool arrived = false;
 #pragma unroll 1
-            for (int c4 = hw; c4 < nch; c4 += NHELP) {
+            for (int c4 = top; c4 >= 0; c4 -= NHELP) {
+              if (!arrived && c4 < nch - 2) {
+                __syncwarp();
+                named_bar_arrive(BAR_X + (sp & 1), PANEL_THREADS);  // sub-panel sp - 2 has all its feedback
+                arrived = true;
+              }
               float acc[4];
 #pragma unroll
               for (int y = 0; y < 4; ++y) acc[y] = sm.As[ab][4 * c4 + y][rr];
@@ -595,8 +606,10 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
 #pragma unroll
               for (int y = 0; y < 4; ++y) sm.As[ab][4 * c4 + y][rr] = acc[y];
             }
-            __syncwarp();
-            named_bar_arrive(BAR_X + (sp & 1), PANEL_THREADS);  // sub-panel sp - 2 has all its in-panel feedback
+            if (!arrived) {
+              __syncwarp();
+              named_bar_arrive(BAR_X + (sp & 1), PANEL_THREADS);
+            }
           }
           TP_ACC(c_x, t4);
           TP_T0(t5);
@@ -667,7 +680,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         asm volatile("cp.async.wait_all;" ::: "memory");  // the next panel's weights are in ws
         fence_proxy_async_global();  // residual digit stores -> visible to the TMA (async proxy)
         named_bar_sync(BAR_PANEL, PANEL_THREADS);
-        if (warp == 7 && lane == 0) {
+        if (warp == 6 && lane == 0) {
           mbar_arrive(&sm.ebar);
           mbar_arrive(&sm.as_free[ab]);
         }
@@ -826,7 +839,7 @@ ganq_status_t launch_t(const float* W, const float* Lhat, const int8_t* LTq, con
             "bar %.1f; sub-panel loads %.1f, column loop %.1f) | helper/warp st %.1f, cross %.1f\n",
             h[0] / c / 1e3, h[1] / c / 1e3, h[2] / c / 1e3, h[3] / c / 1e3, h[4] / c / 1e3, h[5] / c / 1e3,
             h[6] / c / 4e3, h[7] / c / 4e3, h[8] / c / 4e3, h[9] / c / 1e3, h[10] / c / 1e3, h[11] / c / 1e3,
-            h[12] / c / 1e3, h[15] / c / 1e3, h[16] / c / 1e3, h[17] / c / 1e3, h[13] / c / 3e3, h[14] / c / 3e3);
+            h[12] / c / 1e3, h[15] / c / 1e3, h[16] / c / 1e3, h[17] / c / 1e3, h[13] / c / (1e3 * NHELP), h[14] / c / (1e3 * NHELP));
     const unsigned long long z[20] = {};
     cudaMemcpyToSymbol(g_ssprof, z, sizeof(z));
   }

@@ -128,3 +128,40 @@ def test_world2_gloo_matches_single_process():
     Qs, Ts = oracle.quantize(W.numpy().astype(np.float64), H0, nbits, K)
     assert np.array_equal(Q0, Qs)                      # rows are independent (Eq. 2)
     np.testing.assert_array_equal(T0, Ts)
+
+
+def _oracle_quantize_f32(Wloc, H, nbits, iters, **kw):
+    Q, T = _oracle_quantize(Wloc, H, nbits, iters, **kw)
+    return Q, T.float()  # the product's codebook dtype (fp32), as the empty shard's
+
+
+def _worker_fewer_rows(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, n, p, nbits, K = 1, 24, 2 * SC, 2, 2
+        W = synthetic.make_weights(m, n, seed=7)
+        X = synthetic.make_activations(p, n, seed=8)
+        t0, t1 = shard_tokens(p, world, rank, chunk=SC)
+        res = quantize_layer_distributed(W, X[t0:t1].contiguous(), nbits, K, hessian_fns=EMU,
+                                         quantize_fn=_oracle_quantize_f32)
+        out[rank] = (res.Q.numpy(), res.T.numpy(), res.rows)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_gloo_more_ranks_than_rows():
+    """m = 1 < world = 2: rank 1 owns no rows, skips the solve and still joins the collectives
+    (no hang); both ranks end with the one row's (Q, T)."""
+    import oracle
+    oracle.build()
+    world = 2
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker_fewer_rows, args=(world, _free_port(), out), nprocs=world, start_method="spawn",
+                       join=True)
+    Q0, T0, rows0 = out[0]
+    Q1, T1, rows1 = out[1]
+    assert rows0 == (0, 1) and rows1 == (1, 1)
+    assert Q0.shape == (1, 24) and np.array_equal(Q0, Q1) and np.array_equal(T0, T1)
