@@ -156,10 +156,11 @@ lut_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, c
 }
 
 // Fast path for the common shape: N = 4, n a multiple of 256 (whole chunks, 4-byte aligned code
-// words), X 16-byte aligned.  Same arithmetic and summation order as lut_gemm_kernel (a lane's
-// codes in ascending j, fmaf into fp32, then the butterfly), without per-code bounds checks.
+// words), X 16-byte aligned.  fmaf into fp32 in ascending j per lane, split over NA accumulators
+// by the code's position in its word (4 for one token, 2 for two), added in a fixed order, then
+// the butterfly; 4 CTAs per SM (64 registers) so that one launch covers m = 4096 rows in one wave.
 template <int PT>
-__global__ void __launch_bounds__(32 * LUT_WARPS)
+__global__ void __launch_bounds__(32 * LUT_WARPS, PT <= 2 ? 4 : 2)
 lut4_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, const __half* __restrict__ X,
                  int m, int n, int p, float* __restrict__ Y) {
   __shared__ __align__(512) float sT[LUT_WARPS * 16];
@@ -192,21 +193,25 @@ lut4_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, 
   // shared address of this warp's 16 fp32 entries (64-byte aligned), OR-ed with (code * 4): the
   // address of a lookup is one LOP3 of the shifted code word
   const uint32_t tsh = smem_u32(sT) + (uint32_t)warp * 64u;
-  // rows are software-pipelined per warp: the codes of the first LUT_CH chunks and the codebook
-  // entry of the next row are in flight while the current row is computed
+  // one row per warp when m <= the resident warps (the launch is sized for it)
   const int stride = gridDim.x * LUT_WARPS;
   int row = blockIdx.x * LUT_WARPS + warp;
-  for (; row < m; row += stride) {
-    uint32_t b0[LUT_CH];
-#pragma unroll
-    for (int u = 0; u < LUT_CH; ++u) b0[u] = bn[u];
+  for (bool first = true; row < m; row += stride, first = false) {
+    // (the first row's codes and codebook entry were requested before X was staged; later rows
+    // -- only when m exceeds the resident warps -- load theirs here)
+    if (!first) prefetch(row);
+    const uint32_t* b0 = bn;
     if (lane < 16) sT[warp * 16 + lane] = tn;
-    if (row + stride < m) prefetch(row + stride);
     __syncwarp();
     const uint32_t* prow = reinterpret_cast<const uint32_t*>(P + (int64_t)row * rb);
-    float acc[PT];
+    // NA independent accumulators per token (code k of a word -> accumulator k % NA): short
+    // dependent FMA chains, then a fixed-order combine and the butterfly
+    constexpr int NA = PT == 1 ? 4 : (PT == 2 ? 2 : 1);
+    float acc[PT][NA];
 #pragma unroll
-    for (int t = 0; t < PT; ++t) acc[t] = 0.0f;
+    for (int t = 0; t < PT; ++t)
+#pragma unroll
+      for (int a = 0; a < NA; ++a) acc[t][a] = 0.0f;
     for (int c0 = 0; c0 < chunks; c0 += LUT_CH) {
       uint32_t b[LUT_CH];
 #pragma unroll
@@ -228,25 +233,27 @@ lut4_gemm_kernel(const uint8_t* __restrict__ P, const __half* __restrict__ T16, 
         for (int t = 0; t < PT; ++t) {
           const float4* xp = reinterpret_cast<const float4*>(sXf + t * n + 256 * (c0 + u) + 8 * lane);
           const float4 x0 = xp[0], x1 = xp[1];
-          acc[t] = fmaf(w[0], x0.x, acc[t]);
-          acc[t] = fmaf(w[1], x0.y, acc[t]);
-          acc[t] = fmaf(w[2], x0.z, acc[t]);
-          acc[t] = fmaf(w[3], x0.w, acc[t]);
-          acc[t] = fmaf(w[4], x1.x, acc[t]);
-          acc[t] = fmaf(w[5], x1.y, acc[t]);
-          acc[t] = fmaf(w[6], x1.z, acc[t]);
-          acc[t] = fmaf(w[7], x1.w, acc[t]);
+          const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[t][k % NA] = fmaf(w[k], xv[k], acc[t][k % NA]);
         }
       }
+    }
+    float accs[PT];
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {
+      accs[t] = acc[t][0];
+#pragma unroll
+      for (int a = 1; a < NA; ++a) accs[t] = __fadd_rn(accs[t], acc[t][a]);
     }
 #pragma unroll
     for (int t = 0; t < PT; ++t)
 #pragma unroll
-      for (int o = 16; o; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+      for (int o = 16; o; o >>= 1) accs[t] += __shfl_xor_sync(0xffffffffu, accs[t], o);
     if (lane == 0) {
 #pragma unroll
       for (int t = 0; t < PT; ++t)
-        if (t < p) Y[(int64_t)t * m + row] = acc[t];
+        if (t < p) Y[(int64_t)t * m + row] = accs[t];
     }
     __syncwarp();
   }

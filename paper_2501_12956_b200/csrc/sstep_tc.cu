@@ -20,8 +20,8 @@
 // sequential decisions per panel with the in-panel feedback in fp32 FMA, and quantizes each
 // finished 64-column half of residuals for the tensor cores.
 //
-// Warps: 0 = TMA producer, 1 = MMA issuer (+TMEM owner), 2-5 = TMEM readers (one lane
-// quarter each), 6 = decisions (lane = row), 7-11 = in-panel feedback, code and digit stores.
+// Warps (roles below): TMA producer, MMA issuer (+TMEM owner), 4 TMEM readers (one lane quarter
+// each), the decision warp (lane = row), 5 helpers (in-panel feedback, codes, residual digits).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -48,9 +48,16 @@ constexpr uint16_t CMASK = (1u << CS) - 1u;
 constexpr int A_TILE = PW * UB;     // 8 KB: one digit of LhatT (128 panel columns x 64 u)
 constexpr int B_TILE = RB * UB;     // 2 KB: one digit of E (32 rows x 64 u)
 constexpr int STAGE_BYTES = 3 * A_TILE + 3 * B_TILE;  // 30 KB
-constexpr int NHELP = 5;        // in-panel helper warps (6 .. 10)
-constexpr int DECIDE_WARP = 6 + NHELP;     // the highest warp id: first pick of its scheduler
+constexpr int NHELP = 5;        // in-panel helper warps
 constexpr int THREADS = 32 * (7 + NHELP);  // TMA, MMA, 4 readers, helpers, decisions
+// Warp roles (a warp's scheduler = its id % 4; a TMEM reader's lane quarter = its id % 4): the
+// decision warp's scheduler hosts only it, the TMA warp and one reader (the light roles), the
+// helpers share the other three schedulers with the remaining readers.
+constexpr int TMA_WARP = 3, MMA_WARP = 1, READER0 = 4, DECIDE_WARP = 11;
+__host__ __device__ constexpr int helper_index(int w) {  // helpers: warps 0, 2, 8, 9, 10
+  return w == 0 ? 0 : w == 2 ? 1 : w >= 8 && w <= 10 ? w - 6 : -1;
+}
+constexpr int HELPER0 = 0;  // signals the panel-end barriers
 constexpr int PANEL_THREADS = 32 * (1 + NHELP);
 // digit a of LhatT times the E digits b = 0 .. 2 - a: N = 32 (3 - a)
 __host__ __device__ constexpr uint32_t idesc_digit(int a) { return umma_idesc_s8(PW, RB * (3 - a)); }
@@ -152,7 +159,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     mbar_init(&sm.ldbar, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&sm.tmem_slot, 512);
+  if (warp == MMA_WARP) tmem_alloc(&sm.tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // every CTA's barriers exist before any multicast targets them
@@ -160,7 +167,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
   const uint32_t tmem = sm.tmem_slot;
   const uint32_t crank = cluster_ctarank();
 
-  if (warp == 0) {
+  if (warp == TMA_WARP) {
     // ---------------- TMA producer: blocks of target q = 1..P-1, source panels oldest first
     if (lane == 0) {
       // diagonal block of panel 0 (the panel warp waits on ldbar, one phase per panel)
@@ -217,7 +224,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       tp_flush(dbg, 0, 1, w_empty);
       tp_flush(dbg, 0, 2, w_ebar);
     }
-  } else if (warp == 1) {
+  } else if (warp == MMA_WARP) {
     // ---------------- MMA issuer: one accumulator set per block (exact int32 digit sums)
     if (lane == 0) {
       TP_T0(t_all);
@@ -256,7 +263,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       tp_flush(dbg, 0, 4, w_te);
       tp_flush(dbg, 0, 5, w_full);
     }
-  } else if (warp < 6) {
+  } else if (warp >= READER0 && warp < READER0 + 4) {
     // ---------------- TMEM readers: lane = panel column c, 32 fp32 partials (rows)
     const int quarter = warp & 3;
     const int c = quarter * 32 + lane;
@@ -355,7 +362,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     tp_flush(dbg, lane, 7, w_tf);
     tp_flush(dbg, lane, 8, w_af);
   } else {
-    // ---------------- panel group (warps 6-11).  Warp 6 decides (lane = row); warps 7-11 apply
+    // ---------------- panel group: the decision warp (lane = row) and the helpers, which apply
     // the feedback between sub-panels (the next sub-panel's first, handed over by a named
     // barrier), store the codes and quantize finished halves of residuals for the tensor cores.
     const int64_t mq = (m + RB - 1) / RB * RB;  // rows of the sE table
@@ -528,7 +535,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       // ===== helpers: lane = row.  After sub-panel sp is decided, its residuals are applied to
       // every column of sub-panels <= sp - 2 (4-column chunks dealt round-robin to the warps);
       // codes leave in 32-column groups, residual digits in 64-column halves.
-      const int hw = warp - 6;
+      const int hw = helper_index(warp);
       const int rr = lane;
       const int64_t row = r0 + rr;
       const bool live = row < m;
@@ -616,7 +623,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           // the decision warp is past sub-panel sp: stage the next panel's weights there
           if (hw == 2 && q + 1 < P) stage_w(jb - PW, SB * sp);
           const int64_t j32 = jb + SB * sp;  // (when sp % 4 == 0) first column of a 32-group
-          if (hw == 0 && live && (sp & (32 / SB - 1)) == 0) {
+          if (hw == 4 && live && (sp & (32 / SB - 1)) == 0) {
             const int g0 = SB * sp;
             uint32_t pw[8];
 #pragma unroll
@@ -637,50 +644,52 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           // per-row scale and three int8 digits of E (reading R-15); storage column
           // hs = j + (npq - n), a multiple of 64
           const int64_t hs = npq - n + j32;
-          if (hw == 1 && (sp & (64 / SB - 1)) == 0 && q < P - 1 && hs >= 0) {
+          if (hw < 4 && (sp & (64 / SB - 1)) == 0 && q < P - 1 && hs >= 0) {
+            // helper hw digitises the 16 columns [16 hw, 16 hw + 16) of the half (each computes the
+            // half's row maximum itself: the same value on all four)
             const int g0 = SB * sp;
             float mx = 0.0f;
 #pragma unroll 8
             for (int x = 0; x < 64; ++x) mx = fmaxf(mx, fabsf(sm.es[g0 + x][rr]));
             const float scale = (mx > 0.0f) ? mx / QSCALE : 0.0f;
             const float inv = (mx > 0.0f) ? QSCALE / mx : 0.0f;
-#pragma unroll 1
-            for (int x16 = 0; x16 < 4; ++x16) {
-              uint32_t dg[3][4];
+            const int x16 = hw;
+            uint32_t dg[3][4];
 #pragma unroll
-              for (int x4 = 0; x4 < 4; ++x4) {
-                uint32_t w0 = 0, w1 = 0, w2 = 0;
+            for (int x4 = 0; x4 < 4; ++x4) {
+              uint32_t w0 = 0, w1 = 0, w2 = 0;
 #pragma unroll
-                for (int y = 0; y < 4; ++y) {
-                  int h = __float2int_rn(sm.es[g0 + 16 * x16 + 4 * x4 + y][rr] * inv);
-                  const int d2 = ((h + 128) & 255) - 128;
-                  h = (h - d2) >> 8;
-                  const int d1 = ((h + 128) & 255) - 128;
-                  const int d0 = (h - d1) >> 8;
-                  w0 |= (uint32_t)(d0 & 255) << (8 * y);
-                  w1 |= (uint32_t)(d1 & 255) << (8 * y);
-                  w2 |= (uint32_t)(d2 & 255) << (8 * y);
-                }
-                dg[0][x4] = w0;
-                dg[1][x4] = w1;
-                dg[2][x4] = w2;
+              for (int y = 0; y < 4; ++y) {
+                int h = __float2int_rn(sm.es[g0 + 16 * x16 + 4 * x4 + y][rr] * inv);
+                const int d2 = ((h + 128) & 255) - 128;
+                h = (h - d2) >> 8;
+                const int d1 = ((h + 128) & 255) - 128;
+                const int d0 = (h - d1) >> 8;
+                w0 |= (uint32_t)(d0 & 255) << (8 * y);
+                w1 |= (uint32_t)(d1 & 255) << (8 * y);
+                w2 |= (uint32_t)(d2 & 255) << (8 * y);
               }
-              if (live) {
-#pragma unroll
-                for (int d = 0; d < 3; ++d)
-                  *reinterpret_cast<uint4*>(Eq + ((int64_t)d * m + row) * npq + hs + 16 * x16) =
-                      make_uint4(dg[d][0], dg[d][1], dg[d][2], dg[d][3]);
-              }
+              dg[0][x4] = w0;
+              dg[1][x4] = w1;
+              dg[2][x4] = w2;
             }
-            if (live) sE[(hs / UB) * mq + row] = scale;
-            sm.sEn[sp / (64 / SB)][rr] = scale;  // half 0 / 1 of this panel, for the readers
+            if (live) {
+#pragma unroll
+              for (int d = 0; d < 3; ++d)
+                *reinterpret_cast<uint4*>(Eq + ((int64_t)d * m + row) * npq + hs + 16 * x16) =
+                    make_uint4(dg[d][0], dg[d][1], dg[d][2], dg[d][3]);
+            }
+            if (hw == 0) {
+              if (live) sE[(hs / UB) * mq + row] = scale;
+              sm.sEn[sp / (64 / SB)][rr] = scale;  // half 0 / 1 of this panel, for the readers
+            }
           }
           TP_ACC(c_st, t5);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");  // the next panel's weights are in ws
         fence_proxy_async_global();  // residual digit stores -> visible to the TMA (async proxy)
         named_bar_sync(BAR_PANEL, PANEL_THREADS);
-        if (warp == 6 && lane == 0) {
+        if (warp == HELPER0 && lane == 0) {
           mbar_arrive(&sm.ebar);
           mbar_arrive(&sm.as_free[ab]);
         }
@@ -696,7 +705,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
   __syncthreads();
   cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == MMA_WARP) tmem_dealloc(tmem, 512);
 }
 
 // Per layer: Lhat[u][j] = L_uj / L_jj for u > j (fp32, for the in-panel feedback).  Rows have
