@@ -98,9 +98,9 @@ Layout make_layout(int64_t m, int64_t n, int nlev) {
   L.Lhat = take((size_t)n * np * sizeof(float));
   const size_t npq = (size_t)ssq_pitch(n), nblk = npq / 64, mq = ((size_t)m + 31) / 32 * 32;
   L.LTq = take(3 * (size_t)n * npq);               // int8 digits of LhatT (R-15)
-  L.tL = take(nblk * (size_t)n * sizeof(float));   // their per (block, column) scales
+  L.tL = take(nblk * (size_t)n * sizeof(float));   // per-block column maxima, then the column scales
   L.Eq = take(3 * (size_t)m * npq);                // int8 digits of the residuals E
-  L.sE = take(nblk * mq * sizeof(float));          // their per (block, row) scales
+  L.sE = take((align_up((size_t)ss_panels(n) * n, 64) + (size_t)ss_panels(n) * mq) * sizeof(float));  // scales per source panel: LhatT columns, then E rows
   L.hdiag = take((size_t)n * sizeof(double));      // H_jj (T-update right-hand side)
   L.H32 = take(nn * sizeof(float));
   L.WH = take(mn * sizeof(float));
@@ -131,6 +131,9 @@ template <typename T>
 T* at(void* ws, size_t off) {
   return reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + off);
 }
+// the sE region: LhatT scales per (source panel, column), then E scales per (source panel, row)
+float* tlp_of(void* ws, const Layout& L) { return at<float>(ws, L.sE); }
+float* sep_of(void* ws, const Layout& L, int64_t n) { return at<float>(ws, L.sE) + align_up((size_t)ss_panels(n) * n, 64); }
 
 ganq_status_t check_shape(int64_t m, int64_t n, int n_bits) {
   if (m < 1 || n < 1) {
@@ -227,7 +230,10 @@ SideStream& side_stream() {
   int dev = 0;
   cudaGetDevice(&dev);
   if (sd.device != dev) {
-    cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking);
+    // lowest priority: the factorisation's latency-bound panel chain keeps the SMs it asks for
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&sd.s, cudaStreamNonBlocking, lo);
     cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming);
     sd.device = dev;
@@ -544,9 +550,9 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
       GANQ_STAGE(ST_DERIVE);
       if ((s = launch_derive_operands(nullptr, H, n, nullptr, H32, st))) return s;
       if ((s = launch_hdiag(H, n, at<double>(ws, L.hdiag), st))) return s;
-      // block scales of rows >= m are never written but are read (multiplied by zero digits)
-      GANQ_CUDA_TRY(cudaMemsetAsync(at<float>(ws, L.sE), 0,
-                                    (size_t)ssq_pitch(n) / 64 * (((size_t)m + 31) / 32 * 32) * sizeof(float), st));
+      // E scales of rows >= m are never written but are read (multiplied by zero digits)
+      GANQ_CUDA_TRY(cudaMemsetAsync(sep_of(ws, L, n), 0, (size_t)ss_panels(n) * (((size_t)m + 31) / 32 * 32) * sizeof(float),
+                                    st));
       // fixed-point int8 digits of H's strict lower triangle for the tensor-core T-update
       if ((s = launch_tq_prep(H, n, at<int8_t>(ws, L.Hq), at<double>(ws, L.qscale), st))) return s;
     }
@@ -574,7 +580,8 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
   s = factor(H, n, o, ws, L, nullptr, st);
   if (!s) {
     GANQ_STAGE(ST_DERIVE);
-    s = launch_lhat_prep(at<double>(ws, L.A64), n, Lhat, at<int8_t>(ws, L.LTq), at<float>(ws, L.tL), st);
+    s = launch_lhat_prep(at<double>(ws, L.A64), n, Lhat, at<int8_t>(ws, L.LTq), tlp_of(ws, L), at<float>(ws, L.tL),
+                         st);
   }
   // join (also on an error: no side-stream work may outlive the call's use of the workspace)
   GANQ_CUDA_TRY(cudaStreamWaitEvent(st, sd.join, 0));
@@ -583,8 +590,8 @@ ganq_status_t ganq_quantize_layer(const float* W, int64_t m, int64_t n, const do
     {
       // S-update
       GANQ_STAGE(ST_SSTEP);
-      if ((s = launch_sstep_tc(W, Lhat, at<int8_t>(ws, L.LTq), at<float>(ws, L.tL), T, m, n, nlev, Q,
-                               at<int8_t>(ws, L.Eq), at<float>(ws, L.sE), st)))
+      if ((s = launch_sstep_tc(W, Lhat, at<int8_t>(ws, L.LTq), tlp_of(ws, L), T, m, n, nlev, Q,
+                               at<int8_t>(ws, L.Eq), sep_of(ws, L, n), st)))
         return s;
     }
     {

@@ -513,7 +513,10 @@ ganq_status_t launch_cholesky(double* A, int64_t n, int* d_status, int* d_ticket
   GANQ_CUDA_TRY(cudaGetDevice(&dev));
   if (g.device != dev) {
     g = CholGraph();
-    GANQ_CUDA_TRY(cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking));
+    // high priority: the factorisation's panel chain takes SMs ahead of work overlapping it
+    int lo = 0, hi = 0;
+    GANQ_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GANQ_CUDA_TRY(cudaStreamCreateWithPriority(&g.cs, cudaStreamNonBlocking, hi));
     GANQ_CUDA_TRY(cudaEventCreateWithFlags(&g.ev_in, cudaEventDisableTiming));
     GANQ_CUDA_TRY(cudaEventCreateWithFlags(&g.ev_out, cudaEventDisableTiming));
     g.device = dev;

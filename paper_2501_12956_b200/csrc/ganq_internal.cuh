@@ -89,10 +89,15 @@ ganq_status_t launch_tgram_tc(const int8_t* Hq, const double* scale, const uint8
 // sstep_tc.cu
 int64_t ss_pitch(int64_t n);   // fp32 Lhat row pitch (multiple of 4)
 int64_t ssq_pitch(int64_t n);  // int8 digit-plane row pitch (multiple of 64); n_blocks = ssq_pitch / 64
-ganq_status_t launch_lhat_prep(const double* L, int64_t n, float* Lhat, int8_t* LTq, float* tL, cudaStream_t st);
-ganq_status_t launch_sstep_tc(const float* W, const float* Lhat, const int8_t* LTq, const float* tL,
+int64_t ss_panels(int64_t n);  // 128-column panels of the S-step
+// Lhat (fp32, in-panel feedback) and the 24-bit digits of LhatT with their scales per (source
+// panel, column) tLp[ss_panels(n)][n] (bmax: scratch of ssq_pitch(n) / 64 * n floats)
+ganq_status_t launch_lhat_prep(const double* L, int64_t n, float* Lhat, int8_t* LTq, float* tLp, float* bmax,
+                               cudaStream_t st);
+// sEp: the residual digits' scales per (source panel, row), ss_panels(n) x ceil32(m) floats
+ganq_status_t launch_sstep_tc(const float* W, const float* Lhat, const int8_t* LTq, const float* tLp,
                               const float* T, int64_t m, int64_t n, int nlev, uint8_t* Q, int8_t* Eq,
-                              float* sE, cudaStream_t st);
+                              float* sEp, cudaStream_t st);
 // gemm_tc.cu
 int64_t gemm_pitch(int64_t K);
 ganq_status_t launch_split_tf32(const float* X, int64_t rows, int64_t K, float* hi, float* lo,

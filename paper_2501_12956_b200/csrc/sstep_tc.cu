@@ -9,16 +9,17 @@
 // from every column right of it is a dense contraction
 //     A_q[c][r] = sum_u LhatT[jb_q + c][u] * E[r][u]          (M = 128 panel columns,
 //                                                            N = 32 rows, K = u)
-// computed in exact integer arithmetic on tcgen05.mma kind::i8 (reading R-15): per 64-u block
-// both operands are 24-bit fixed point with their own scale (LhatT per (column, block), E per
-// (row, block)), split into three balanced int8 digits; the six digit products of weight
-// >= 2^16 are exact int32 sums: one MMA per LhatT digit against the stacked E digits (N = 96,
-// 64, 32), offset so that equal weights (2^32, 2^24, 2^16) accumulate in the same columns.  The
-// reader warps scale each block's integer sums and add them in fp32 registers.  Blocks are
+// computed in exact integer arithmetic on tcgen05.mma kind::i8 (reading R-15): per SOURCE PANEL
+// (128 u) both operands are 24-bit fixed point with their own scale (LhatT per (column, source
+// panel), E per (row, source panel)), split into three balanced int8 digits; the six digit
+// products of weight >= 2^16 are exact int32 sums: one MMA per LhatT digit against the stacked
+// E digits (N = 96, 64, 32), offset so that equal weights (2^32, 2^24, 2^16) accumulate in the
+// same columns.  The two 64-u blocks of a source panel accumulate in one TMEM set; the reader
+// warps scale each source panel's integer sums and add them in fp32 registers.  Blocks are
 // issued oldest first, so the feedback of panel q-1 runs while panel q is still being decided;
 // only its last 2 blocks wait for panel q's residuals.  The panel group makes the 128
-// sequential decisions per panel with the in-panel feedback in fp32 FMA, and quantizes each
-// finished 64-column half of residuals for the tensor cores.
+// sequential decisions per panel with the in-panel feedback in fp32 FMA, and quantizes the
+// finished panel's residuals for the tensor cores.
 //
 // Warps (roles below): TMA producer, MMA issuer (+TMEM owner), 4 TMEM readers (one lane quarter
 // each), the decision warp (lane = row), 5 helpers (in-panel feedback, codes, residual digits).
@@ -41,7 +42,7 @@ constexpr int SB = 8;               // decision sub-panel width
 constexpr int NSUB = PW / SB;
 constexpr int UB = 64;              // u per feedback block (64-byte SW64 rows of int8 digits)
 constexpr int STAGES = 3;
-constexpr int NBUF = 4;             // TMEM accumulator sets of 3 x 32 columns (weight groups)
+constexpr int NBUF = 4;             // TMEM accumulator sets of 3 x 32 columns (one per source panel)
 constexpr int BUF_COLS = 3 * RB;
 constexpr int CS = 4;               // cluster size: row groups sharing each LhatT tile (multicast)
 constexpr uint16_t CMASK = (1u << CS) - 1u;
@@ -62,13 +63,14 @@ constexpr int PANEL_THREADS = 32 * (1 + NHELP);
 // digit a of LhatT times the E digits b = 0 .. 2 - a: N = 32 (3 - a)
 __host__ __device__ constexpr uint32_t idesc_digit(int a) { return umma_idesc_s8(PW, RB * (3 - a)); }
 constexpr float QSCALE = 8388608.0f - 65536.0f;  // 2^23 - 2^16: |fixed-point value| bound
+
 struct SsSmem {
   alignas(128) float Ld[PW][PW];         // Lhat[jb + c][jb + c2] of the current panel (TMA)
   alignas(16) float As[2][PW][RB + 1];   // drained feedback per (panel column, row), 2 buffers
   alignas(16) float es[PW][RB + 1];      // residuals of the current panel (column, row)
   alignas(16) uint8_t cs[PW][RB + 4];    // codes of the current panel (column, row)
+  alignas(16) float sEn[RB];             // E scales of the newest source panel (rows)
   alignas(16) float ws[PW][RB + 1];      // weights of the current panel (column, row)
-  alignas(16) float sEn[2][RB];          // E block scales of the newest source panel (2 halves)
   alignas(8) uint64_t full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF];
   alignas(8) uint64_t acc_ready[2], as_free[2], ebar, ldbar;
   uint32_t tmem_slot;
@@ -135,10 +137,10 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 template <int NLEV>
 __global__ void __launch_bounds__(THREADS, 1)
 sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant__ CUtensorMap tmE,
-                const __grid_constant__ CUtensorMap tmLd, const float* __restrict__ tL,
+                const __grid_constant__ CUtensorMap tmLd, const float* __restrict__ tLp,
                 const float* __restrict__ W, const float* __restrict__ T, int64_t m, int64_t n,
                 int64_t np, int64_t npq, uint8_t* __restrict__ Q, int8_t* __restrict__ Eq,
-                float* __restrict__ sE, int dbg) {
+                float* __restrict__ sEp, int dbg) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -225,24 +227,27 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       tp_flush(dbg, 0, 2, w_ebar);
     }
   } else if (warp == MMA_WARP) {
-    // ---------------- MMA issuer: one accumulator set per block (exact int32 digit sums)
+    // ---------------- MMA issuer: one accumulator set per source panel (exact int32 digit sums)
     if (lane == 0) {
       TP_T0(t_all);
       long long w_te = 0, w_full = 0;
       uint32_t kb = 0;
+      uint32_t dr = 0;  // drains (source panels) so far
       for (int q = 1; q < P; ++q)
-        for (int qs = 0; qs < q; ++qs)
+        for (int qs = 0; qs < q; ++qs, ++dr) {
+          const uint32_t buf = dr % NBUF;
+          TP_T0(t0);
+          mbar_wait(&sm.tempty[buf], ((dr / NBUF) & 1) ^ 1);
+          TP_ACC(w_te, t0);
+          tc_fence_after();
+          const uint32_t d = tmem + buf * BUF_COLS;
           for (int k2 = 0; k2 < PW / UB; ++k2, ++kb) {
-            const uint32_t s = kb % STAGES, buf = kb % NBUF;
-            TP_T0(t0);
-            mbar_wait(&sm.tempty[buf], ((kb / NBUF) & 1) ^ 1);
-            TP_ACC(w_te, t0);
+            const uint32_t s = kb % STAGES;
             TP_T0(t1);
             mbar_wait(&sm.full[s], (kb / STAGES) & 1);
             TP_ACC(w_full, t1);
             tc_fence_after();
             const uint32_t st = smem_u32(tiles + s * STAGE_BYTES);
-            const uint32_t d = tmem + buf * BUF_COLS;
             // one MMA per LhatT digit a against the stacked E digits [b0; b1; ...; b_{2-a}]
             // (N = 32 (3 - a)) written from column 32 a, so that product (a, b) lands in column
             // range a + b: the tensor core adds equal weights (2^32, 2^24, 2^16) in exact int32,
@@ -253,10 +258,11 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
               for (int dg = 0; dg < 3; ++dg)
                 mma_i8(d + dg * RB, umma_desc_sw64(st + dg * A_TILE + kk * 32),
                        umma_desc_sw64(st + 3 * A_TILE + kk * 32), idesc_digit(dg),
-                       (kk == 0 && dg == 0) ? 0u : 1u);
+                       (k2 == 0 && kk == 0 && dg == 0) ? 0u : 1u);
             mma_commit_mc(&sm.empty[s], CMASK);  // frees stage s in every CTA of the cluster
-            mma_commit(&sm.tfull[buf]);
           }
+          mma_commit(&sm.tfull[buf]);  // the source panel's sums are complete
+        }
       long long tot = 0;
       TP_ACC(tot, t_all);
       tp_flush(dbg, 0, 3, tot);
@@ -264,30 +270,28 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       tp_flush(dbg, 0, 5, w_full);
     }
   } else if (warp >= READER0 && warp < READER0 + 4) {
-    // ---------------- TMEM readers: lane = panel column c, 32 fp32 partials (rows)
+    // ---------------- TMEM readers: lane = panel column c, 32 fp32 feedback values (rows)
     const int quarter = warp & 3;
     const int c = quarter * 32 + lane;
-    uint32_t kb = 0;
     TP_T0(t_all);
     long long w_tf = 0, w_af = 0;
+    const int64_t mq = (m + RB - 1) / RB * RB;  // rows of the sEp table
+    uint32_t dr = 0;
     for (int q = 0; q < P; ++q) {
       const int64_t j = n - (int64_t)PW * (q + 1) + c;  // this lane's panel column (< 0: phantom)
       float acc[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) acc[r] = 0.0f;
-      // block scales: LhatT per (column, block), E per (row, block); the digit weights of the
-      // three groups are 2^32, 2^24, 2^16 = 2^16 x (65536, 256, 1).  Scales of older source panels
-      // are loaded one block ahead (the readers may run behind the MMA, so a load issued right
-      // before its tfull wait would not be hidden); those of the newest source panel (qs = q - 1)
-      // come from the panel group's shared copy after tfull (ordered after its stores by ebar ->
-      // TMA -> MMA -> commit).
-      const int nblkq = q * (PW / UB);
-      auto load_scales = [&](int i, float& tl_o, float (&se_o)[RB]) {
-        const int qs = i / (PW / UB), k2 = i % (PW / UB);
-        const int64_t blk = (npq - (int64_t)PW * (qs + 1)) / UB + k2;  // storage block of u
-        tl_o = __ldg(tL + blk * n + (j >= 0 ? j : 0));  // raw: consumed a block later
+      // scales: LhatT per (column, source panel), E per (row, source panel); the digit weights of
+      // the three groups are 2^32, 2^24, 2^16 = 2^16 x (65536, 256, 1).  Scales of older source
+      // panels are loaded one drain ahead (the readers may run behind the MMA, so a load issued
+      // right before its tfull wait would not be hidden); those of the newest source panel
+      // (qs = q - 1) come from the panel group's shared copy after tfull (ordered after its stores
+      // by ebar -> TMA -> MMA -> commit).
+      auto load_scales = [&](int qs, float& tl_o, float (&se_o)[RB]) {
+        tl_o = __ldg(tLp + (int64_t)qs * n + (j >= 0 ? j : 0));
         if (qs != q - 1) {
-          const float4* sp4 = reinterpret_cast<const float4*>(sE + blk * ((m + RB - 1) / RB * RB) + r0);
+          const float4* sp4 = reinterpret_cast<const float4*>(sEp + (int64_t)qs * mq + r0);
 #pragma unroll
           for (int r4 = 0; r4 < RB / 4; ++r4) {
             const float4 v4 = sp4[r4];
@@ -299,51 +303,43 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         }
       };
       float tl_n = 0.0f, se_n[RB];
-      if (nblkq > 0) load_scales(0, tl_n, se_n);
-      for (int i = 0; i < nblkq; ++i, ++kb) {
-        {
-          const uint32_t buf = kb % NBUF;
-          const int k2 = i % (PW / UB);
-          const bool newest = (i / (PW / UB) == q - 1);
-          const float tl = tl_n;
-          float se[RB];
+      if (q > 0) load_scales(0, tl_n, se_n);
+      for (int qs = 0; qs < q; ++qs, ++dr) {
+        const uint32_t buf = dr % NBUF;
+        const float tl = tl_n;
+        float se[RB];
 #pragma unroll
-          for (int r = 0; r < RB; ++r) se[r] = se_n[r];
-          if (i + 1 < nblkq) load_scales(i + 1, tl_n, se_n);
-          TP_T0(t0);
-          mbar_wait(&sm.tfull[buf], (kb / NBUF) & 1);
-          TP_ACC(w_tf, t0);
-          tc_fence_after();
-          if (newest) {
+        for (int r = 0; r < RB; ++r) se[r] = se_n[r];
+        if (qs + 1 < q) load_scales(qs + 1, tl_n, se_n);
+        TP_T0(t0);
+        mbar_wait(&sm.tfull[buf], (dr / NBUF) & 1);
+        TP_ACC(w_tf, t0);
+        tc_fence_after();
+        if (qs == q - 1) {
 #pragma unroll
-            for (int r = 0; r < RB; ++r) se[r] = sm.sEn[k2][r];
+          for (int r = 0; r < RB; ++r) se[r] = sm.sEn[r];
+        }
+        const float tls = (j >= 0) ? tl * 65536.0f : 0.0f;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) se[r] *= tls;
+        const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BUF_COLS;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // rows [16 hh, 16 hh + 16): three weight groups
+          uint32_t c0[16], c1[16], c2[16];
+          tmem_ld16(tb + 16 * hh, c0);
+          tmem_ld16(tb + RB + 16 * hh, c1);
+          tmem_ld16(tb + 2 * RB + 16 * hh, c2);
+          tmem_ld_wait();
+          if (hh == 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.tempty[buf]);
           }
-          const float tls = (j >= 0) ? tl * 65536.0f : 0.0f;
 #pragma unroll
-          for (int r = 0; r < RB; ++r) se[r] *= tls;
-          const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + buf * BUF_COLS;
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {  // rows [16 hh, 16 hh + 16): three weight groups
-            uint32_t c0[16], c1[16], c2[16];
-            tmem_ld16(tb + 16 * hh, c0);
-            tmem_ld16(tb + RB + 16 * hh, c1);
-            tmem_ld16(tb + 2 * RB + 16 * hh, c2);
-            tmem_ld_wait();
-            if (hh == 1) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&sm.tempty[buf]);
-            }
-#pragma unroll
-            for (int x = 0; x < 16; ++x) {
-              // |digit-group sums| < 3 * 64 * 2^14 < 2^22: exact int -> float by the 1.5 * 2^23
-              // bias (IADD + FADD on the full-rate pipes instead of the conversion unit)
-              const float f0 = __fsub_rn(__int_as_float((int)c0[x] + 0x4B400000), 12582912.0f);
-              const float f1 = __fsub_rn(__int_as_float((int)c1[x] + 0x4B400000), 12582912.0f);
-              const float f2 = __fsub_rn(__int_as_float((int)c2[x] + 0x4B400000), 12582912.0f);
-              const float v = fmaf(f0, 65536.0f, fmaf(f1, 256.0f, f2));
-              acc[16 * hh + x] = fmaf(v, se[16 * hh + x], acc[16 * hh + x]);
-            }
+          for (int x = 0; x < 16; ++x) {
+            // exact int32 sums (< 3 * 128 * 2^14 < 2^23) -> fp32, combined by weight
+            const float v = fmaf((float)(int)c0[x], 65536.0f, fmaf((float)(int)c1[x], 256.0f, (float)(int)c2[x]));
+            acc[16 * hh + x] = fmaf(v, se[16 * hh + x], acc[16 * hh + x]);
           }
         }
       }
@@ -365,7 +361,6 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     // ---------------- panel group: the decision warp (lane = row) and the helpers, which apply
     // the feedback between sub-panels (the next sub-panel's first, handed over by a named
     // barrier), store the codes and quantize finished halves of residuals for the tensor cores.
-    const int64_t mq = (m + RB - 1) / RB * RB;  // rows of the sE table
     // named barriers: the panel end, and per sub-panel parity (the decision warp may run two
     // sub-panels ahead of the helpers and vice versa, so each id has one open phase at most)
     constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_X = 6, BAR_HELP = 8;  // ES: 4, 5; X: 6, 7
@@ -640,48 +635,50 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
                 if (j32 + x >= 0) qd[x] = (uint8_t)(pw[x >> 2] >> (8 * (x & 3)));
             }
           }
-          // a finished 64-column half of a source panel (the leftmost panel is never one):
-          // per-row scale and three int8 digits of E (reading R-15); storage column
-          // hs = j + (npq - n), a multiple of 64
-          const int64_t hs = npq - n + j32;
-          if (hw < 4 && (sp & (64 / SB - 1)) == 0 && q < P - 1 && hs >= 0) {
-            // helper hw digitises the 16 columns [16 hw, 16 hw + 16) of the half (each computes the
-            // half's row maximum itself: the same value on all four)
-            const int g0 = SB * sp;
+          // a finished panel (the leftmost panel is never a source): per-row scale and three int8
+          // digits of E (reading R-15) at storage columns j + (npq - n)
+          if (hw < 4 && sp == 0 && q < P - 1) {
+            // the finished panel (a source of every panel left of it): the row's scale max |e| /
+            // QSCALE over its 128 columns (each helper computes it: the same value) and the
+            // digits; helper hw digitises the 32 columns [32 hw, 32 hw + 32)
             float mx = 0.0f;
 #pragma unroll 8
-            for (int x = 0; x < 64; ++x) mx = fmaxf(mx, fabsf(sm.es[g0 + x][rr]));
+            for (int x = 0; x < PW; ++x) mx = fmaxf(mx, fabsf(sm.es[x][rr]));
             const float scale = (mx > 0.0f) ? mx / QSCALE : 0.0f;
             const float inv = (mx > 0.0f) ? QSCALE / mx : 0.0f;
-            const int x16 = hw;
-            uint32_t dg[3][4];
+            const int64_t hp = npq - n + jb;  // storage column of the panel's first column
+#pragma unroll 1
+            for (int x16 = 2 * hw; x16 < 2 * hw + 2; ++x16) {
+              if (hp + 16 * x16 < 0) continue;  // phantom columns (zero-filled by the TMA)
+              uint32_t dg[3][4];
 #pragma unroll
-            for (int x4 = 0; x4 < 4; ++x4) {
-              uint32_t w0 = 0, w1 = 0, w2 = 0;
+              for (int x4 = 0; x4 < 4; ++x4) {
+                uint32_t w0 = 0, w1 = 0, w2 = 0;
 #pragma unroll
-              for (int y = 0; y < 4; ++y) {
-                int h = __float2int_rn(sm.es[g0 + 16 * x16 + 4 * x4 + y][rr] * inv);
-                const int d2 = ((h + 128) & 255) - 128;
-                h = (h - d2) >> 8;
-                const int d1 = ((h + 128) & 255) - 128;
-                const int d0 = (h - d1) >> 8;
-                w0 |= (uint32_t)(d0 & 255) << (8 * y);
-                w1 |= (uint32_t)(d1 & 255) << (8 * y);
-                w2 |= (uint32_t)(d2 & 255) << (8 * y);
+                for (int y = 0; y < 4; ++y) {
+                  int h = __float2int_rn(sm.es[16 * x16 + 4 * x4 + y][rr] * inv);
+                  const int d2 = ((h + 128) & 255) - 128;
+                  h = (h - d2) >> 8;
+                  const int d1 = ((h + 128) & 255) - 128;
+                  const int d0 = (h - d1) >> 8;
+                  w0 |= (uint32_t)(d0 & 255) << (8 * y);
+                  w1 |= (uint32_t)(d1 & 255) << (8 * y);
+                  w2 |= (uint32_t)(d2 & 255) << (8 * y);
+                }
+                dg[0][x4] = w0;
+                dg[1][x4] = w1;
+                dg[2][x4] = w2;
               }
-              dg[0][x4] = w0;
-              dg[1][x4] = w1;
-              dg[2][x4] = w2;
-            }
-            if (live) {
+              if (live) {
 #pragma unroll
-              for (int d = 0; d < 3; ++d)
-                *reinterpret_cast<uint4*>(Eq + ((int64_t)d * m + row) * npq + hs + 16 * x16) =
-                    make_uint4(dg[d][0], dg[d][1], dg[d][2], dg[d][3]);
+                for (int d = 0; d < 3; ++d)
+                  *reinterpret_cast<uint4*>(Eq + ((int64_t)d * m + row) * npq + hp + 16 * x16) =
+                      make_uint4(dg[d][0], dg[d][1], dg[d][2], dg[d][3]);
+              }
             }
             if (hw == 0) {
-              if (live) sE[(hs / UB) * mq + row] = scale;
-              sm.sEn[sp / (64 / SB)][rr] = scale;  // half 0 / 1 of this panel, for the readers
+              if (live) sEp[(int64_t)q * ((m + RB - 1) / RB * RB) + row] = scale;
+              sm.sEn[rr] = scale;  // the newest source panel's scales, for the readers
             }
           }
           TP_ACC(c_st, t5);
@@ -720,12 +717,18 @@ __global__ void lhat_kernel(const double* __restrict__ L, int64_t n, int64_t np,
   }
 }
 
-// Per layer: LhatT[j][u] = L_uj / L_jj (u > j) as 24-bit fixed point per (column j, 64-u block):
-// tL[blk][j] = max_{u in blk} |LhatT[j][u]| / (2^23 - 2^16) and three balanced int8 digits
-// LTq[d][j][u'] (digit 0 on top) at right-aligned storage columns u' = u + (npq - n), npq a
-// multiple of 64 (reading R-15).  One CTA per (32 columns j, one block of 64 u).
+// Per layer: LhatT[j][u] = L_uj / L_jj (u > j, u in a source panel of j) as 24-bit fixed point per
+// (column j, source panel qs) (reading R-15): tLp[qs][j] = max |LhatT[j][u]| / (2^23 - 2^16) over
+// the panel's u, and three balanced int8 digits LTq[d][j][u'] (digit 0 on top) at right-aligned
+// storage columns u' = u + (npq - n), npq a multiple of 64; source panel qs covers the storage
+// columns [npq - 128 (qs + 1), npq - 128 qs).  One CTA per (32 columns j, one block of 64 u); pass 0
+// writes each block's column maxima into bmax[blk][j], lhat_panelmax_kernel combines the two
+// blocks of each panel into tLp, pass 1 writes the digits.
+__device__ __forceinline__ int64_t panel_of_block(int64_t blk, int64_t npq) { return (npq / 64 - 1 - blk) / 2; }
+
 __global__ void __launch_bounds__(256) lhat_quant_kernel(const double* __restrict__ L, int64_t n, int64_t npq,
-                                                         int8_t* __restrict__ LTq, float* __restrict__ tL) {
+                                                         int8_t* __restrict__ LTq, float* __restrict__ bmax,
+                                                         const float* __restrict__ tLp, int pass) {
   __shared__ double tile[64][33];
   const int64_t j0 = (int64_t)blockIdx.x * 32;
   const int64_t blk = blockIdx.y;
@@ -740,17 +743,24 @@ __global__ void __launch_bounds__(256) lhat_quant_kernel(const double* __restric
     }
   }
   __syncthreads();
-  constexpr double QS = 8388608.0 - 65536.0;
   for (int jj = 0; jj < 4; ++jj) {
     const int jl = ty * 4 + jj;
     const int64_t j = j0 + jl;
     if (j >= n) break;
-    const double x0 = tile[tx][jl], x1 = tile[tx + 32][jl];
-    double mx = fmax(fabs(x0), fabs(x1));
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const float sc = (mx > 0.0) ? (float)(mx / QS) : 0.0f;
-    const double inv = (mx > 0.0) ? 1.0 / (double)sc : 0.0;
-    if (tx == 0) tL[blk * n + j] = sc;
+    // only the source panels of column j (right of its own panel: storage u' >= npq - 128 q_j) go
+    // through the tensor cores; the in-panel entries (the largest, near the diagonal) are applied
+    // in fp32 and are neither scaled nor stored here
+    const int64_t qj = (n - 1 - j) / 128;
+    const bool src = blk * 64 >= npq - 128 * qj;
+    const double x0 = src ? tile[tx][jl] : 0.0, x1 = src ? tile[tx + 32][jl] : 0.0;
+    if (pass == 0) {
+      double mx = fmax(fabs(x0), fabs(x1));
+      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (tx == 0) bmax[blk * n + j] = (float)mx;
+      continue;
+    }
+    const float sc = tLp[panel_of_block(blk, npq) * n + j];
+    const double inv = (sc > 0.0f) ? 1.0 / (double)sc : 0.0;
     const double xs[2] = {x0, x1};
     for (int h2 = 0; h2 < 2; ++h2) {
       long long h = llrint(xs[h2] * inv);
@@ -764,6 +774,18 @@ __global__ void __launch_bounds__(256) lhat_quant_kernel(const double* __restric
       LTq[(2 * n + j) * npq + col] = (int8_t)d2;
     }
   }
+}
+
+// tLp[qs][j] = the max of panel qs's two blocks (storage blocks npq/64 - 2 qs - 1, - 2) / QSCALE,
+// rounded up so that every |x| / tLp <= 2^23 - 2^16 (a block index < 0 is a phantom block: 0)
+__global__ void lhat_panelmax_kernel(const float* __restrict__ bmax, int64_t n, int64_t npq, float* __restrict__ tLp) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t qs = blockIdx.y;
+  if (j >= n) return;
+  const int64_t b1 = npq / 64 - 1 - 2 * qs, b0 = b1 - 1;
+  float mx = (b1 >= 0) ? bmax[b1 * n + j] : 0.0f;
+  if (b0 >= 0) mx = fmaxf(mx, bmax[b0 * n + j]);
+  tLp[qs * n + j] = (mx > 0.0f) ? __fdiv_ru(mx, QSCALE) * (1.0f + 0x1p-22f) : 0.0f;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -807,8 +829,8 @@ bool make_digit_map(CUtensorMap* map, const int8_t* base, int64_t npq, int64_t o
 }
 
 template <int NLEV>
-ganq_status_t launch_t(const float* W, const float* Lhat, const int8_t* LTq, const float* tL, const float* T,
-                       int64_t m, int64_t n, int64_t np, int64_t npq, uint8_t* Q, int8_t* Eq, float* sE,
+ganq_status_t launch_t(const float* W, const float* Lhat, const int8_t* LTq, const float* tLp, const float* T,
+                       int64_t m, int64_t n, int64_t np, int64_t npq, uint8_t* Q, int8_t* Eq, float* sEp,
                        cudaStream_t st) {
   CUtensorMap mLT, mE, mLd;
   // out-of-range boxes (rows >= m, panel columns < 0) are zero-filled by the TMA
@@ -834,8 +856,8 @@ ganq_status_t launch_t(const float* W, const float* Lhat, const int8_t* LTq, con
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   static const int dbg = getenv("GANQ_SSTEP_DBG") ? atoi(getenv("GANQ_SSTEP_DBG")) : 0;
-  GANQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, sstep_tc_kernel<NLEV>, mLT, mE, mLd, tL, W, T, m, n, np, npq, Q,
-                                   Eq, sE, dbg));
+  GANQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, sstep_tc_kernel<NLEV>, mLT, mE, mLd, tLp, W, T, m, n, np, npq, Q,
+                                   Eq, sEp, dbg));
   GANQ_LAUNCH_CHECK("sstep_tc_kernel");
   if (dbg & 16) {
     unsigned long long h[20];
@@ -860,24 +882,32 @@ ganq_status_t launch_t(const float* W, const float* Lhat, const int8_t* LTq, con
 int64_t ss_pitch(int64_t n) { return (n + 3) / 4 * 4; }
 int64_t ssq_pitch(int64_t n) { return (n + 63) / 64 * 64; }
 
-ganq_status_t launch_lhat_prep(const double* L, int64_t n, float* Lhat, int8_t* LTq, float* tL, cudaStream_t st) {
+int64_t ss_panels(int64_t n) { return (n + 127) / 128; }
+
+ganq_status_t launch_lhat_prep(const double* L, int64_t n, float* Lhat, int8_t* LTq, float* tLp, float* bmax,
+                               cudaStream_t st) {
   const int64_t np = ss_pitch(n), npq = ssq_pitch(n);
   lhat_kernel<<<dim3((unsigned)((np + 255) / 256), (unsigned)n), 256, 0, st>>>(L, n, np, Lhat);
   GANQ_LAUNCH_CHECK("lhat_kernel");
-  lhat_quant_kernel<<<dim3((unsigned)((n + 31) / 32), (unsigned)(npq / 64)), 256, 0, st>>>(L, n, npq, LTq, tL);
+  const dim3 grid((unsigned)((n + 31) / 32), (unsigned)(npq / 64));
+  lhat_quant_kernel<<<grid, 256, 0, st>>>(L, n, npq, LTq, bmax, tLp, 0);
+  GANQ_LAUNCH_CHECK("lhat_quant_kernel");
+  lhat_panelmax_kernel<<<dim3((unsigned)((n + 255) / 256), (unsigned)ss_panels(n)), 256, 0, st>>>(bmax, n, npq, tLp);
+  GANQ_LAUNCH_CHECK("lhat_panelmax_kernel");
+  lhat_quant_kernel<<<grid, 256, 0, st>>>(L, n, npq, LTq, bmax, tLp, 1);
   GANQ_LAUNCH_CHECK("lhat_quant_kernel");
   return GANQ_OK;
 }
 
-ganq_status_t launch_sstep_tc(const float* W, const float* Lhat, const int8_t* LTq, const float* tL,
+ganq_status_t launch_sstep_tc(const float* W, const float* Lhat, const int8_t* LTq, const float* tLp,
                               const float* T, int64_t m, int64_t n, int nlev, uint8_t* Q, int8_t* Eq,
-                              float* sE, cudaStream_t st) {
+                              float* sEp, cudaStream_t st) {
   const int64_t np = ss_pitch(n), npq = ssq_pitch(n);
   switch (nlev) {
-    case 2: return launch_t<2>(W, Lhat, LTq, tL, T, m, n, np, npq, Q, Eq, sE, st);
-    case 4: return launch_t<4>(W, Lhat, LTq, tL, T, m, n, np, npq, Q, Eq, sE, st);
-    case 8: return launch_t<8>(W, Lhat, LTq, tL, T, m, n, np, npq, Q, Eq, sE, st);
-    case 16: return launch_t<16>(W, Lhat, LTq, tL, T, m, n, np, npq, Q, Eq, sE, st);
+    case 2: return launch_t<2>(W, Lhat, LTq, tLp, T, m, n, np, npq, Q, Eq, sEp, st);
+    case 4: return launch_t<4>(W, Lhat, LTq, tLp, T, m, n, np, npq, Q, Eq, sEp, st);
+    case 8: return launch_t<8>(W, Lhat, LTq, tLp, T, m, n, np, npq, Q, Eq, sEp, st);
+    case 16: return launch_t<16>(W, Lhat, LTq, tLp, T, m, n, np, npq, Q, Eq, sEp, st);
     default:
       set_error(GANQ_ERR_UNSUPPORTED, "sstep: %d levels unsupported", nlev);
       return GANQ_ERR_UNSUPPORTED;

@@ -198,8 +198,9 @@ def test_sstep_teacher_forced(m, n, p, nbits, policy):
     Tk = torch.from_numpy(oracle.init_codebook(W.numpy(), nbits)).to(DEV)
     for k in range(4):
         Qg, Tn = g.quantize_layer(Wd, H, nbits, 1, precond=policy, lam=lam, T0=Tk)
-        mism, bad, _ = audit(W.numpy(), L, Tk.cpu().numpy(), Qg.cpu().numpy())
-        assert bad == 0, f"iteration {k}: {bad} code decisions beyond the near-tie tolerance"
+        mism, bad, ratio = audit(W.numpy(), L, Tk.cpu().numpy(), Qg.cpu().numpy())
+        print(f"\n[P-3 {m}x{n} N={nbits} {policy} k={k}] {mism} near-ties, max margin {ratio:.2e} max|T|")
+        assert bad == 0, f"iteration {k}: {bad} code decisions beyond the near-tie tolerance (max margin {ratio:.2e})"
         assert mism <= max(2, 0.001 * m * n)
         Tk = Tn
 
