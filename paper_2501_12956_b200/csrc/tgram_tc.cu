@@ -50,7 +50,7 @@ constexpr int THREADS = 448;                     // 14 warps
 constexpr int A_COL0 = 3 * TJ;                   // TMEM: 3 accumulators, then the A ring
 constexpr int A_COLS = TK / 4;                   // 32 columns of 4 int8 per stage
 constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile (sorting unit)
-constexpr uint32_t IDESC = umma_idesc_u8s8(128, TJ);  // A = one-hot bytes 0 / 128 (u8)
+constexpr uint32_t IDESC = umma_idesc_u8s8(128, TJ);  // A = one-hot bytes 0 / 1 (u8)
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
 
 // debug-only cycle accounting per warp role: compiled with -DGANQ_KPROF, enabled at run time
@@ -98,8 +98,10 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   const int64_t r0 = (int64_t)(blockIdx.x % gp) * R;
   const int NT = (int)((n + TJ - 1) / TJ);
   const int part = blockIdx.x / gp;
-  const int bnd[SPLIT + 1] = {0, jsplit.x, jsplit.y, jsplit.z, NT};
-  const int jt_lo = bnd[part], jt_hi = bnd[part + 1];
+  const bool small_sums = n <= 32768;  // every int32 digit sum fits the add-only conversion
+  static_assert(SPLIT == 4, "j ranges come from jsplit.x .. z");
+  const int jt_lo = part == 0 ? 0 : part == 1 ? jsplit.x : part == 2 ? jsplit.y : jsplit.z;
+  const int jt_hi = part == 0 ? jsplit.x : part == 1 ? jsplit.y : part == 2 ? jsplit.z : NT;
   double* Cpart = Cg + (size_t)part * (size_t)m * NLEV * NLEV;
 
   if (threadIdx.x == 0) {
@@ -133,10 +135,10 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
           TP_ACC(w_empty, t0);
           uint8_t* st = tiles + s * STAGE_BYTES;
-          mbar_arrive_expect_tx(&sm.full[s], 3 * B_TILE);
+          const int nl = (dbg & 32) ? 1 : 3;  // debug: load one digit tile only (timing probe)
+          mbar_arrive_expect_tx(&sm.full[s], nl * B_TILE);
           // this CTA's slice of j rows of each digit tile, multicast to the whole cluster
-#pragma unroll
-          for (int l = 0; l < 3; ++l)
+          for (int l = 0; l < nl; ++l)
             tma_load_2d_mc(st + l * B_TILE + crank * SLICE * TK, &tmap, &sm.full[s], kt * TK,
                            (int)(l * P + jt * TJ + crank * SLICE), CMASK);
         }
@@ -146,41 +148,39 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       tp_flush(dbg, 0, 1, w_empty);
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
+    // ---------------- MMA issuer (the whole warp waits; one elected lane issues each stage)
+    {
       TP_T0(t_all);
       long long w_full = 0, w_tempty = 0;
-      uint32_t ks = 0;
+      uint32_t s = 0, ph = 0;
+      const uint64_t desc0 = umma_desc_sw128(smem_u32(tiles), 16, 1024);
       for (int jt = jt_lo; jt < jt_hi; ++jt) {
         TP_T0(t1);
         mbar_wait(&sm.tempty, ((jt - jt_lo) & 1) ^ 1);
         TP_ACC(w_tempty, t1);
         tc_fence_after();
-        for (int kt = 0; kt < ktiles_of(jt); ++kt, ++ks) {
-          const uint32_t s = ks % STAGES;
+        const int nk = ktiles_of(jt);
+        for (int kt = 0; kt < nk; ++kt) {
           TP_T0(t0);
-          mbar_wait(&sm.full[s], (ks / STAGES) & 1);
+          mbar_wait(&sm.full[s], ph);
           TP_ACC(w_full, t0);
           tc_fence_after();
-          const uint32_t s_addr = smem_u32(tiles + s * STAGE_BYTES);
-          const uint32_t a_tmem = tmem + A_COL0 + s * A_COLS;
-#pragma unroll
-          for (int l = 0; l < 3; ++l) {
-            const uint32_t b_addr = s_addr + l * B_TILE;
-#pragma unroll
-            for (int kk = 0; kk < TK / 32; ++kk)
-              if (!(dbg & 8)) mma_i8_ts(tmem + l * TJ, a_tmem + kk * 8, umma_desc_sw128(b_addr + kk * 32, 16, 1024), IDESC,
-                        (kt > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit_mc(&sm.empty[s], CMASK);  // frees stage s in every CTA of the cluster
+          __syncwarp();
+          if (!(dbg & 8))
+            mma_i8_ts_stage12_mc(tmem, tmem + A_COL0 + s * A_COLS, desc0 + (uint64_t)(s * (STAGE_BYTES >> 4)),
+                                 IDESC, kt == 0 ? 1u : 0u, &sm.empty[s], CMASK);
+          else if (lane == 0)
+            mma_commit_mc(&sm.empty[s], CMASK);  // frees stage s in every CTA of the cluster
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        mma_commit(&sm.tfull);
+        __syncwarp();
+        if (lane == 0) mma_commit(&sm.tfull);
       }
       long long tot = 0;
       TP_ACC(tot, t_all);
-      tp_flush(dbg, 0, 2, tot);
-      tp_flush(dbg, 0, 3, w_full);
-      tp_flush(dbg, 0, 4, w_tempty);
+      tp_flush(dbg, lane, 2, tot);
+      tp_flush(dbg, lane, 3, w_full);
+      tp_flush(dbg, lane, 4, w_tempty);
     }
   } else if (warp < 6) {
     // ---------------- one-hot producers: TMEM lane (i, b) <- [q_ik == b] for the stage's 64 k
@@ -212,10 +212,11 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     };
     // byte-wise (x == b) -> 0x80 / 0x00 for codes < 16 or 0xFF (no borrow crosses a byte):
     // y = (x ^ b) | 0x80 per byte; its low 7 bits are zero iff x == b, so ~(y - 1) keeps bit 7
-    // exactly then.  The factor 128 of the u8 operand is divided out with the scale s_j.
+    // exactly then; shifted down to 0x01 (a unit one-hot keeps every digit sum below 2^22 for
+    // n <= 32768, the range of the epilogue's add-only int -> float conversion)
     auto onehot = [&](uint32_t x) {
       const uint32_t y = (x ^ bb) | 0x80808080u;
-      return (0x01010100u - y) & 0x80808080u;  // == ~(y - 0x01010101) & 0x80808080
+      return ((0x01010100u - y) & 0x80808080u) >> 7;  // == (~(y - 0x01010101) & 0x80808080) >> 7
     };
     int jt = jt_lo, kt = 0, nk = ktiles_of(jt_lo);
     uint32_t s = 0, ph = 0;
@@ -290,34 +291,38 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       TP_T0(ta);
       // (1) sorted order of each row's 32-column chunks (counting sort by code); overlaps MMA
       constexpr int NTASK = (R * NCH + 7) / 8;
-      int codes[NTASK];
+      constexpr int UB8 = NTASK < 8 ? NTASK : 8;  // tasks whose codes are loaded together
 #pragma unroll
-      for (int u = 0; u < NTASK; ++u) {
-        const int task = e + 8 * u;
-        const int ri = task / NCH, c = task % NCH;
-        const int64_t row = r0 + ri, j = J0 + c * 32 + lane;
-        codes[u] = (task < R * NCH && row < m && j < n) ? (int)__ldg(Q + row * n + j) : 0xFF;
-      }
+      for (int u0 = 0; u0 < NTASK; u0 += UB8) {
+        int codes[UB8];
 #pragma unroll
-      for (int u = 0; u < NTASK; ++u) {
-        const int task = e + 8 * u;
-        if (task >= R * NCH) break;
-        const int ri = task / NCH, c = task % NCH;
-        const int code = codes[u];
-        const unsigned lt = (1u << lane) - 1u;
-        int base = 0, pos = -1;
-#pragma unroll
-        for (int a = 0; a < NLEV; ++a) {
-          const unsigned bal = __ballot_sync(0xffffffffu, code == a);
-          if (lane == 0) sm.off[ri][c][a] = (uint8_t)base;
-          if (code == a) pos = base + __popc(bal & lt);
-          base += __popc(bal);
+        for (int u = 0; u < UB8; ++u) {
+          const int task = e + 8 * (u0 + u);
+          const int ri = task / NCH, c = task % NCH;
+          const int64_t row = r0 + ri, j = J0 + c * 32 + lane;
+          codes[u] = (task < R * NCH && row < m && j < n) ? (int)__ldg(Q + row * n + j) : 0xFF;
         }
-        if (lane == 0) sm.off[ri][c][NLEV] = (uint8_t)base;
-        // invalid columns (j >= n, rows >= m) go after every segment
-        sm.ipos[ri][c * 32 + lane] = (uint8_t)(pos >= 0 ? pos : 31);
+#pragma unroll
+        for (int u = 0; u < UB8; ++u) {
+          const int task = e + 8 * (u0 + u);
+          if (task >= R * NCH) break;
+          const int ri = task / NCH, c = task % NCH;
+          const int code = codes[u];
+          const unsigned lt = (1u << lane) - 1u;
+          int base = 0, pos = -1;
+#pragma unroll
+          for (int a = 0; a < NLEV; ++a) {
+            const unsigned bal = __ballot_sync(0xffffffffu, code == a);
+            if (lane == 0) sm.off[ri][c][a] = (uint8_t)base;
+            if (code == a) pos = base + __popc(bal & lt);
+            base += __popc(bal);
+          }
+          if (lane == 0) sm.off[ri][c][NLEV] = (uint8_t)base;
+          // invalid columns (j >= n, rows >= m) go after every segment
+          sm.ipos[ri][c * 32 + lane] = (uint8_t)(pos >= 0 ? pos : 31);
+        }
       }
-      if (h == 0) sm.scale[et] = (J0 + et < n) ? (float)(scale[J0 + et] * (1.0 / 128.0)) : 0.0f;
+      if (h == 0) sm.scale[et] = (J0 + et < n) ? (float)scale[J0 + et] : 0.0f;
       named_bar_sync(1, EPI_THREADS);
       TP_ACC(e_sort, ta);
       TP_T0(tb0);
@@ -333,13 +338,40 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         tmem_ld16(tb, d0);
         tmem_ld16(tb + TJ, d1);
         tmem_ld16(tb + 2 * TJ, d2);
-        tmem_ld_wait();
+        // the 16 sorted positions and scales of these columns, loaded before any staging store
+        // (vector loads; no shared-memory load waits between the stores)
+        const uint4 ip4 = *reinterpret_cast<const uint4*>(&sm.ipos[i][g * 16]);
+        float sc[16];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          const float v = fmaf((float)(int)d0[t], 65536.0f,
-                               fmaf((float)(int)d1[t], 256.0f, (float)(int)d2[t]));
-          const int x = g * 16 + t;  // write in sorted order within its 32-column chunk
-          sm.stage[et][(x & ~31) + sm.ipos[i][x]] = v * sm.scale[x];
+        for (int t4 = 0; t4 < 4; ++t4) {
+          const float4 s4 = reinterpret_cast<const float4*>(&sm.scale[g * 16])[t4];
+          sc[4 * t4 + 0] = s4.x;
+          sc[4 * t4 + 1] = s4.y;
+          sc[4 * t4 + 2] = s4.z;
+          sc[4 * t4 + 3] = s4.w;
+        }
+        const uint32_t ipw[4] = {ip4.x, ip4.y, ip4.z, ip4.w};
+        float* srow = &sm.stage[et][(g * 16) & ~31];
+        tmem_ld_wait();
+        if (small_sums) {
+          // |digit sum| <= 128 (n - 1) < 2^22: exact conversion by adding to 1.5 * 2^23 in the
+          // integer domain and subtracting it in fp32 (full-rate IADD + FADD instead of I2F)
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23 == __int_as_float(0x4B400000)
+            const float f0 = __int_as_float((int)d0[t] + 0x4B400000) - MAGIC;
+            const float f1 = __int_as_float((int)d1[t] + 0x4B400000) - MAGIC;
+            const float f2 = __int_as_float((int)d2[t] + 0x4B400000) - MAGIC;
+            const float v = fmaf(f0, 65536.0f, fmaf(f1, 256.0f, f2));
+            srow[(ipw[t >> 2] >> (8 * (t & 3))) & 0xFF] = v * sc[t];  // sorted order in its chunk
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const float v = fmaf((float)(int)d0[t], 65536.0f,
+                                 fmaf((float)(int)d1[t], 256.0f, (float)(int)d2[t]));
+            srow[(ipw[t >> 2] >> (8 * (t & 3))) & 0xFF] = v * sc[t];
+          }
         }
       }
       tc_fence_before();
