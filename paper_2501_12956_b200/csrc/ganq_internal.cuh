@@ -302,54 +302,105 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
 }
 // One pipeline stage of the one-hot T-update contraction, issued by ONE elected lane of a
 // converged warp in a single asm block: for digit l = 0..2 and k-step kk = 0..3,
-//   D[d_tmem + 128 l] (+)= A[a_tmem + 8 kk] * B[bdesc + (l * 16384 + 32 kk) bytes]
+//   D[d_tmem + 128 l] (+)= A[a_tmem + 8 kk] * B[bdesc + (l * DIG + 32 kk) bytes]
 // (kind::i8, A from TMEM), then the MMAs' completion arrives on `bar` in every CTA of `mask`.
 // `first` != 0 overwrites each accumulator with its kk = 0 product.  Issuing the twelve MMAs
 // under one elect.sync (descriptors advanced by immediates) keeps the issuer's instruction
-// chain per MMA shorter than the 64-cycle MMA itself.
-__device__ __forceinline__ void mma_i8_ts_stage12_mc(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
-                                                     uint32_t idesc, uint32_t first, uint64_t* bar,
-                                                     uint16_t mask) {
+// chain per MMA shorter than the 64-cycle MMA itself.  DIG = the byte stride of the digit tiles
+// (16 KB single CTA, 8 KB per CTA of a pair); CG = cta_group.
+#define GANQ_STAGE12(NAME, CG, D1, D2)                                                                    \
+  __device__ __forceinline__ void NAME(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, \
+                                       uint32_t first, uint64_t* bar, uint16_t mask) {                   \
+    asm volatile(                                                                                        \
+        "{\n\t"                                                                                          \
+        ".reg .pred e, acc;\n\t"                                                                         \
+        ".reg .b32 d1, d2, a1, a2, a3;\n\t"                                                              \
+        ".reg .b64 b;\n\t"                                                                               \
+        "elect.sync _|e, 0xffffffff;\n\t"                                                                \
+        "setp.eq.b32 acc, %4, 0;\n\t"                                                                    \
+        "add.u32 d1, %0, 128;\n\t"                                                                       \
+        "add.u32 d2, %0, 256;\n\t"                                                                       \
+        "add.u32 a1, %1, 8;\n\t"                                                                         \
+        "add.u32 a2, %1, 16;\n\t"                                                                        \
+        "add.u32 a3, %1, 24;\n\t"                                                                        \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [%0], [%1], %2, %3, acc;\n\t"                         \
+        "add.s64 b, %2, " D1 ";\n\t"                                                                     \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [d1], [%1], b, %3, acc;\n\t"                          \
+        "add.s64 b, %2, " D2 ";\n\t"                                                                     \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [d2], [%1], b, %3, acc;\n\t"                          \
+        "add.s64 b, %2, 2;\n\t"                                                                          \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [%0], [a1], b, %3, 1;\n\t"                            \
+        "add.s64 b, %2, " D1 "+2;\n\t"                                                                   \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [d1], [a1], b, %3, 1;\n\t"                            \
+        "add.s64 b, %2, " D2 "+2;\n\t"                                                                   \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [d2], [a1], b, %3, 1;\n\t"                            \
+        "add.s64 b, %2, 4;\n\t"                                                                          \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [%0], [a2], b, %3, 1;\n\t"                            \
+        "add.s64 b, %2, " D1 "+4;\n\t"                                                                   \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [d1], [a2], b, %3, 1;\n\t"                            \
+        "add.s64 b, %2, " D2 "+4;\n\t"                                                                   \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [d2], [a2], b, %3, 1;\n\t"                            \
+        "add.s64 b, %2, 6;\n\t"                                                                          \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [%0], [a3], b, %3, 1;\n\t"                            \
+        "add.s64 b, %2, " D1 "+6;\n\t"                                                                   \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [d1], [a3], b, %3, 1;\n\t"                            \
+        "add.s64 b, %2, " D2 "+6;\n\t"                                                                   \
+        "@e tcgen05.mma.cta_group::" CG ".kind::i8 [d2], [a3], b, %3, 1;\n\t"                            \
+        "@e tcgen05.commit.cta_group::" CG                                                               \
+        ".mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t"                    \
+        "}\n" ::"r"(d_tmem),                                                                             \
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(first), "r"(smem_u32(bar)), "h"(mask)                   \
+        : "memory");                                                                                     \
+  }
+// The same stage with A from shared memory (K-major SW128, 128-byte rows: kk advances the
+// A descriptor by 32 bytes), for a CTA pair: cta_group::2, B digit tiles 8 KB apart.
+__device__ __forceinline__ void mma_i8_ss_stage12_pair_mc(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                          uint32_t idesc, uint32_t first, uint64_t* bar,
+                                                          uint16_t mask) {
   asm volatile(
       "{\n\t"
       ".reg .pred e, acc;\n\t"
-      ".reg .b32 d1, d2, a1, a2, a3;\n\t"
-      ".reg .b64 b;\n\t"
+      ".reg .b32 d1, d2;\n\t"
+      ".reg .b64 a, b;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "setp.eq.b32 acc, %4, 0;\n\t"
       "add.u32 d1, %0, 128;\n\t"
       "add.u32 d2, %0, 256;\n\t"
-      "add.u32 a1, %1, 8;\n\t"
-      "add.u32 a2, %1, 16;\n\t"
-      "add.u32 a3, %1, 24;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, acc;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, acc;\n\t"
+      "add.s64 b, %2, 512;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [d1], %1, b, %3, acc;\n\t"
       "add.s64 b, %2, 1024;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], [%1], b, %3, acc;\n\t"
-      "add.s64 b, %2, 2048;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], [%1], b, %3, acc;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [d2], %1, b, %3, acc;\n\t"
+      "add.s64 a, %1, 2;\n\t"
       "add.s64 b, %2, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a, b, %3, 1;\n\t"
+      "add.s64 b, %2, 514;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [d1], a, b, %3, 1;\n\t"
       "add.s64 b, %2, 1026;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], [a1], b, %3, 1;\n\t"
-      "add.s64 b, %2, 2050;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], [a1], b, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [d2], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 4;\n\t"
       "add.s64 b, %2, 4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a2], b, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a, b, %3, 1;\n\t"
+      "add.s64 b, %2, 516;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [d1], a, b, %3, 1;\n\t"
       "add.s64 b, %2, 1028;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], [a2], b, %3, 1;\n\t"
-      "add.s64 b, %2, 2052;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], [a2], b, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [d2], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 6;\n\t"
       "add.s64 b, %2, 6;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a3], b, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a, b, %3, 1;\n\t"
+      "add.s64 b, %2, 518;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [d1], a, b, %3, 1;\n\t"
       "add.s64 b, %2, 1030;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d1], [a3], b, %3, 1;\n\t"
-      "add.s64 b, %2, 2054;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::i8 [d2], [a3], b, %3, 1;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [d2], a, b, %3, 1;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t"
       "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(first), "r"(smem_u32(bar)), "h"(mask)
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(first), "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
+// descriptor units are 16 bytes: 16 KB = 1024, 8 KB = 512
+GANQ_STAGE12(mma_i8_ts_stage12_mc, "1", "1024", "2048")
+GANQ_STAGE12(mma_i8_ts_stage12_pair_mc, "2", "512", "1024")
+#undef GANQ_STAGE12
 // shared memory -> TMEM copy of a 128-row x 32-byte matrix (smem descriptor as for an MMA
 // operand) into 8 consecutive TMEM columns of lanes 0-127; ordered with the issuing thread's
 // later tcgen05.mma like any tcgen05 operation of the same thread.

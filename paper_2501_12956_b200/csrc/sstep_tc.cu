@@ -487,15 +487,18 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
                 if (4 * k4 + 3 < cc - 1) a[4 * k4 + 3] = fmaf(ec, l.w, a[4 * k4 + 3]);
               }
             }
-            // ... and into the next sub-panel
+            // ... and into the next sub-panel (paired FMAs)
             if (sp > 0) {
+              const float2 ee = make_float2(ec, ec);
 #pragma unroll
               for (int k4 = 0; k4 < SB / 4; ++k4) {
                 const float4 l = ln[k4];
-                a2[4 * k4 + 0] = fmaf(ec, l.x, a2[4 * k4 + 0]);
-                a2[4 * k4 + 1] = fmaf(ec, l.y, a2[4 * k4 + 1]);
-                a2[4 * k4 + 2] = fmaf(ec, l.z, a2[4 * k4 + 2]);
-                a2[4 * k4 + 3] = fmaf(ec, l.w, a2[4 * k4 + 3]);
+                float2 p01 = __ffma2_rn(ee, make_float2(l.x, l.y), make_float2(a2[4 * k4 + 0], a2[4 * k4 + 1]));
+                float2 p23 = __ffma2_rn(ee, make_float2(l.z, l.w), make_float2(a2[4 * k4 + 2], a2[4 * k4 + 3]));
+                a2[4 * k4 + 0] = p01.x;
+                a2[4 * k4 + 1] = p01.y;
+                a2[4 * k4 + 2] = p23.x;
+                a2[4 * k4 + 3] = p23.y;
               }
             }
             if (cc > 0) {
@@ -594,19 +597,20 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
                 named_bar_arrive(BAR_X + (sp & 1), PANEL_THREADS);  // sub-panel sp - 2 has all its feedback
                 arrived = true;
               }
-              float acc[4];
-#pragma unroll
-              for (int y = 0; y < 4; ++y) acc[y] = sm.As[ab][4 * c4 + y][rr];
+              // paired fp32 FMAs (FFMA2: two independent round-to-nearest FMAs, the same bits)
+              float2 a01 = make_float2(sm.As[ab][4 * c4][rr], sm.As[ab][4 * c4 + 1][rr]);
+              float2 a23 = make_float2(sm.As[ab][4 * c4 + 2][rr], sm.As[ab][4 * c4 + 3][rr]);
 #pragma unroll
               for (int cc = 0; cc < SB; ++cc) {
                 const float4 l = *reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][4 * c4]);
-                acc[0] = fmaf(e8[cc], l.x, acc[0]);
-                acc[1] = fmaf(e8[cc], l.y, acc[1]);
-                acc[2] = fmaf(e8[cc], l.z, acc[2]);
-                acc[3] = fmaf(e8[cc], l.w, acc[3]);
+                const float2 ee = make_float2(e8[cc], e8[cc]);
+                a01 = __ffma2_rn(ee, make_float2(l.x, l.y), a01);
+                a23 = __ffma2_rn(ee, make_float2(l.z, l.w), a23);
               }
-#pragma unroll
-              for (int y = 0; y < 4; ++y) sm.As[ab][4 * c4 + y][rr] = acc[y];
+              sm.As[ab][4 * c4][rr] = a01.x;
+              sm.As[ab][4 * c4 + 1][rr] = a01.y;
+              sm.As[ab][4 * c4 + 2][rr] = a23.x;
+              sm.As[ab][4 * c4 + 3][rr] = a23.y;
             }
             if (!arrived) {
               __syncwarp();

@@ -39,9 +39,6 @@ namespace {
 
 constexpr int TJ = 128;          // j per tile (UMMA N)
 constexpr int TK = 128;          // k per stage (128-byte swizzle rows of int8)
-constexpr int STAGES = 3;
-constexpr int B_TILE = TJ * TK;                  // 16 KB digit tile of H
-constexpr int STAGE_BYTES = 3 * B_TILE;          // 48 KB (the one-hot A operand lives in TMEM)
 constexpr int SPLIT = 4;                         // CTAs per row group (balanced j ranges)
 constexpr int CS = 2;                            // cluster: CS row groups share every H tile
 constexpr uint16_t CMASK = (1u << CS) - 1;
@@ -50,8 +47,29 @@ constexpr int THREADS = 448;                     // 14 warps
 constexpr int A_COL0 = 3 * TJ;                   // TMEM: 3 accumulators, then the A ring
 constexpr int A_COLS = TK / 4;                   // 32 columns of 4 int8 per stage
 constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile (sorting unit)
-constexpr uint32_t IDESC = umma_idesc_u8s8(128, TJ);  // A = one-hot bytes 0 / 1 (u8)
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
+constexpr int SROW = TJ + 4;                     // staging row pitch (16-byte aligned rows)
+
+// Two forms of the contraction (PAIR selects):
+//  * single CTA: M = 128 (i, b) lanes per CTA; the cluster's two CTAs share every H tile by
+//    multicast, each holding all 128 j rows of it (3 x 16 KB per stage, 3 stages);
+//  * CTA pair (cta_group::2): one MMA covers both CTAs' 256 (i, b) lanes; each CTA holds only its
+//    64-row half of the j tile (3 x 8 KB per stage), halving the bytes every SM's shared memory
+//    takes in per MMA, and its one-hot A rows in shared memory (16 KB per stage, written by the
+//    producers with plain stores: no TMEM stores competing with the MMAs' accumulator traffic).
+template <bool PAIR>
+struct TgCfg {
+  static constexpr int STAGES = 3;
+  static constexpr int BROWS = PAIR ? TJ / 2 : TJ;  // j rows of a digit tile in this CTA
+  static constexpr int B_TILE = BROWS * TK;
+  // single CTA: the one-hot A operand lives in a TMEM ring (tcgen05.st); pair: in shared memory
+  // after the three B digit tiles (128 rows x 128 k, K-major SW128), read by the MMA directly
+  static constexpr int A_TILE = PAIR ? 128 * TK : 0;
+  static constexpr int STAGE_BYTES = 3 * B_TILE + A_TILE;
+  static constexpr uint32_t IDESC = umma_idesc_u8s8(PAIR ? 256 : 128, TJ);  // A = one-hot 0 / 1 (u8)
+};
+static_assert(A_COL0 + TgCfg<true>::STAGES * A_COLS <= 512 && A_COL0 + TgCfg<false>::STAGES * A_COLS <= 512,
+              "accumulators and the A ring fit TMEM");
 
 // debug-only cycle accounting per warp role: compiled with -DGANQ_KPROF, enabled at run time
 // by GANQ_TGRAM_DBG & 16 (tools/tg_prof.sh); absent from the default build
@@ -67,13 +85,15 @@ __device__ __forceinline__ void tp_flush(int dbg, int lane, int slot, long long 
   if ((dbg & 16) && lane == 0) atomicAdd(&g_tgprof[slot], (unsigned long long)v);
 }
 
-template <int NLEV>
+template <int NLEV, int STAGES>
 struct TcSmem {
   static constexpr int R = 128 / NLEV;
-  alignas(16) float stage[128][TJ + 1];      // drained Dt tile (fp32 values), row = (i,b)
-  alignas(16) uint8_t ipos[R][TJ];           // per (row, 32-chunk): sorted position of each j
-  alignas(16) float scale[TJ];               // s_j of the current j-tile (fp32)
-  alignas(16) uint8_t off[R][NCH][NLEV + 1]; // segment offsets per (row, chunk, level)
+  static constexpr int NLEVP = NLEV < 4 ? 4 : NLEV;
+  alignas(16) float stage[128][SROW];         // drained Dt tile (fp32 values), row = (i,b)
+  // double-buffered per j-tile (the sort of tile t + 1 runs while other warps walk tile t)
+  alignas(16) uint8_t ipos[2][R][TJ];         // per (row, 32-chunk): sorted position of each j
+  alignas(16) float scale[2][TJ];             // s_j of the j-tile (fp32)
+  alignas(16) uint8_t oend[2][R][NCH][NLEVP]; // end of each level's segment per (row, chunk)
   alignas(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
   uint32_t tmem_slot;
 };
@@ -81,16 +101,18 @@ struct TcSmem {
 __host__ __device__ inline int ktiles_of(int jt) { return (jt * TJ + TJ - 1) / TK + 1; }
 static_assert(TJ % TK == 0, "producers step ktiles_of by TJ / TK");
 
-template <int NLEV>
+template <int NLEV, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
 tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ Q,
                 const double* __restrict__ scale, int64_t m, int64_t n, int64_t P,
                 const int4 jsplit, int gp, double* __restrict__ Cg, int dbg) {
   constexpr int R = 128 / NLEV;
+  using Cfg = TgCfg<PAIR>;
+  constexpr int STAGES = Cfg::STAGES, B_TILE = Cfg::B_TILE, STAGE_BYTES = Cfg::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  TcSmem<NLEV>& sm = *reinterpret_cast<TcSmem<NLEV>*>(tiles + STAGES * STAGE_BYTES);
+  TcSmem<NLEV, STAGES>& sm = *reinterpret_cast<TcSmem<NLEV, STAGES>*>(tiles + STAGES * STAGE_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // blockIdx.x = part * gp + group (gp = groups rounded up to whole clusters): the CS CTAs of a
@@ -104,23 +126,32 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   const int jt_hi = part == 0 ? jsplit.x : part == 1 ? jsplit.y : part == 2 ? jsplit.z : NT;
   double* Cpart = Cg + (size_t)part * (size_t)m * NLEV * NLEV;
 
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;  // PAIR: the CTA that issues the pair's MMAs
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&sm.full[s], 1 + 4);  // TMA bytes (all CS slices) + one arrive per producer warp
-      mbar_init(&sm.empty[s], CS);    // one (multicast) MMA commit from every CTA of the cluster
+      if (PAIR) {
+        mbar_init(&sm.full[s], 1 + 8);  // (leader's) TMA bytes of both CTAs + both CTAs' producer warps
+        mbar_init(&sm.empty[s], 1);     // the leader's multicast commit
+      } else {
+        mbar_init(&sm.full[s], 1 + 4);  // TMA bytes (all CS slices) + one arrive per producer warp
+        mbar_init(&sm.empty[s], CS);    // one (multicast) MMA commit from every CTA of the cluster
+      }
     }
     mbar_init(&sm.tfull, 1);
-    mbar_init(&sm.tempty, 8);
+    mbar_init(&sm.tempty, PAIR ? 16 : 8);  // PAIR: the leader's counts both CTAs' epilogue warps
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(&sm.tmem_slot, 512);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair(&sm.tmem_slot, 512);
+    else tmem_alloc(&sm.tmem_slot, 512);
+  }
   tc_fence_before();
   __syncthreads();
-  cluster_sync_all();  // every CTA's barriers exist before any multicast targets them
+  cluster_sync_all();  // every CTA's barriers exist before any multicast or remote signal
   tc_fence_after();
   const uint32_t tmem = sm.tmem_slot;
-  const uint32_t crank = cluster_ctarank();
 
   if (warp == 0) {
     // ---------------- TMA: three digit tiles of H per stage
@@ -136,11 +167,19 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           TP_ACC(w_empty, t0);
           uint8_t* st = tiles + s * STAGE_BYTES;
           const int nl = (dbg & 32) ? 1 : 3;  // debug: load one digit tile only (timing probe)
-          mbar_arrive_expect_tx(&sm.full[s], nl * B_TILE);
-          // this CTA's slice of j rows of each digit tile, multicast to the whole cluster
-          for (int l = 0; l < nl; ++l)
-            tma_load_2d_mc(st + l * B_TILE + crank * SLICE * TK, &tmap, &sm.full[s], kt * TK,
-                           (int)(l * P + jt * TJ + crank * SLICE), CMASK);
+          if (PAIR) {
+            // this CTA's 64-row half of each digit tile, counted on the leader's barrier
+            if (leader) mbar_arrive_expect_tx(&sm.full[s], 2 * nl * B_TILE);
+            for (int l = 0; l < nl; ++l)
+              tma_load_2d_pair(st + l * B_TILE, &tmap, &sm.full[s], kt * TK,
+                               (int)(l * P + jt * TJ + crank * SLICE));
+          } else {
+            mbar_arrive_expect_tx(&sm.full[s], nl * B_TILE);
+            // this CTA's slice of j rows of each digit tile, multicast to the whole cluster
+            for (int l = 0; l < nl; ++l)
+              tma_load_2d_mc(st + l * B_TILE + crank * SLICE * TK, &tmap, &sm.full[s], kt * TK,
+                             (int)(l * P + jt * TJ + crank * SLICE), CMASK);
+          }
         }
       long long tot = 0;
       TP_ACC(tot, t_all);
@@ -148,8 +187,9 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       tp_flush(dbg, 0, 1, w_empty);
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (the whole warp waits; one elected lane issues each stage)
-    {
+    // ---------------- MMA issuer (the whole warp waits; one elected lane issues each stage;
+    // PAIR: the leader's warp only)
+    if (!PAIR || leader) {
       TP_T0(t_all);
       long long w_full = 0, w_tempty = 0;
       uint32_t s = 0, ph = 0;
@@ -166,15 +206,28 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           TP_ACC(w_full, t0);
           tc_fence_after();
           __syncwarp();
-          if (!(dbg & 8))
-            mma_i8_ts_stage12_mc(tmem, tmem + A_COL0 + s * A_COLS, desc0 + (uint64_t)(s * (STAGE_BYTES >> 4)),
-                                 IDESC, kt == 0 ? 1u : 0u, &sm.empty[s], CMASK);
-          else if (lane == 0)
-            mma_commit_mc(&sm.empty[s], CMASK);  // frees stage s in every CTA of the cluster
+          const uint64_t bd = desc0 + (uint64_t)(s * (STAGE_BYTES >> 4));
+          const uint32_t at = tmem + A_COL0 + s * A_COLS;
+          // the commit frees stage s in every CTA of the cluster
+          if (dbg & 8) {
+            if (lane == 0) {
+              if (PAIR) mma_commit_pair_mc(&sm.empty[s], CMASK);
+              else mma_commit_mc(&sm.empty[s], CMASK);
+            }
+          } else if (PAIR) {
+            (void)at;
+            mma_i8_ss_stage12_pair_mc(tmem, bd + (uint64_t)((3 * B_TILE) >> 4), bd, Cfg::IDESC, kt == 0 ? 1u : 0u,
+                                      &sm.empty[s], CMASK);
+          } else {
+            mma_i8_ts_stage12_mc(tmem, at, bd, Cfg::IDESC, kt == 0 ? 1u : 0u, &sm.empty[s], CMASK);
+          }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         __syncwarp();
-        if (lane == 0) mma_commit(&sm.tfull);
+        if (lane == 0) {
+          if (PAIR) mma_commit_pair_mc(&sm.tfull, CMASK);  // both CTAs' accumulators are ready
+          else mma_commit(&sm.tfull);
+        }
       }
       long long tot = 0;
       TP_ACC(tot, t_all);
@@ -222,12 +275,13 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     uint32_t s = 0, ph = 0;
     TP_T0(t_all);
     long long w_empty = 0, w_st = 0;
-    // one stage: codes of this stage in cur (loaded a stage ago), prefetch the next into nxt
-    auto stage = [&](const uint4 (&cur)[TK / 16], uint4 (&nxt)[TK / 16]) -> bool {
+    // one stage: codes of this stage in cur (loaded a stage ago), prefetch the next into nxt;
+    // build the one-hot words, wait for the slot and issue its TMEM stores (not yet waited on)
+    auto issue = [&](const uint4 (&cur)[TK / 16], uint4 (&nxt)[TK / 16], uint32_t& slot) -> bool {
       if (jt >= jt_hi) return false;
       int jn = jt, kn = kt + 1;
       if (kn >= nk) { ++jn; kn = 0; }
-      if (jn < jt_hi && !(dbg & 2)) load_codes(kn, nxt);
+      if (jn < jt_hi && !(dbg & 66)) load_codes(kn, nxt);  // dbg & 64: timing probe without code loads
       uint32_t v[TK / 4];
 #pragma unroll
       for (int c = 0; c < TK / 16; ++c) {
@@ -240,31 +294,59 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       mbar_wait(&sm.empty[s], ph ^ 1);
       TP_ACC(w_empty, t0);
       tc_fence_after();
-      TP_T0(t2);
       if (!(dbg & 2)) {
-        const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS;
+        if constexpr (PAIR) {
+          // row pl of the stage's A tile, 16-byte chunk c at (c ^ (pl & 7)) (128-byte swizzle)
+          uint8_t* arow = tiles + s * STAGE_BYTES + 3 * B_TILE + pl * TK;
 #pragma unroll
-        for (int h16 = 0; h16 < TK / 64; ++h16) {
-          uint32_t w16[16];
+          for (int c = 0; c < TK / 16; ++c)
+            *reinterpret_cast<uint4*>(arow + ((c ^ (pl & 7)) << 4)) =
+                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        } else {
+          const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS;
 #pragma unroll
-          for (int x = 0; x < 16; ++x) w16[x] = v[16 * h16 + x];
-          tmem_st16(ta + 16 * h16, w16);
+          for (int h16 = 0; h16 < TK / 64; ++h16) {
+            uint32_t w16[16];
+#pragma unroll
+            for (int x = 0; x < 16; ++x) w16[x] = v[16 * h16 + x];
+            tmem_st16(ta + 16 * h16, w16);
+          }
         }
-        tmem_st_wait();
       }
-      TP_ACC(w_st, t2);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.full[s]);
+      slot = s;
       if (jn != jt) nk += TJ / TK;  // ktiles_of(jt + 1) = ktiles_of(jt) + TJ / TK
       jt = jn;
       kt = kn;
       if (++s == STAGES) { s = 0; ph ^= 1; }
       return true;
     };
+    // publish a stage once its stores are complete (publishing two stages per wait was measured
+    // slower: stage s then waits for stage s + 1's slot)
+    auto publish = [&](uint32_t s0, uint32_t s1, bool two) {
+      TP_T0(t2);
+      if constexpr (PAIR) fence_proxy_async_smem();  // generic stores -> the MMA's (async) reads
+      else tmem_st_wait();
+      TP_ACC(w_st, t2);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (!PAIR || leader) {
+          mbar_arrive(&sm.full[s0]);
+          if (two) mbar_arrive(&sm.full[s1]);
+        } else {  // the leader's MMAs read this CTA's A slots
+          mbar_arrive_remote(&sm.full[s0], 0);
+          if (two) mbar_arrive_remote(&sm.full[s1], 0);
+        }
+      }
+    };
     uint4 ca[TK / 16], cb[TK / 16];
     if (jt < jt_hi) load_codes(kt, ca);
-    while (stage(ca, cb) && stage(cb, ca)) {
+    for (;;) {
+      uint32_t s0 = 0;
+      if (!issue(ca, cb, s0)) break;
+      publish(s0, 0, false);
+      if (!issue(cb, ca, s0)) break;
+      publish(s0, 0, false);
     }
     {
       long long tot = 0;
@@ -285,45 +367,58 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
 #pragma unroll
     for (int a = 0; a < NLEV; ++a) acc[a] = 0.0;
     TP_T0(t_all);
-    long long e_sort = 0, e_wait = 0, e_drain = 0, e_walk = 0, e_bar = 0;
+    long long e_sort = 0, e_wait = 0, e_drain = 0, e_walk = 0, e_bar = 0;  // e_bar: unused
+    // (1) codes of a j-tile: task u of this warp = (row ri, 32-column chunk c); prefetched one
+    //     tile ahead (NTASK <= 8) so that their global-load latency overlaps the walk
+    constexpr int NTASK = (R * NCH + 7) / 8;
+    constexpr bool PREFETCH = NTASK <= 8;
+    constexpr int NCODE = PREFETCH ? NTASK : 1;
+    auto load_codes = [&](int jt, int u) -> int {
+      const int task = e + 8 * u;
+      const int ri = task / NCH, c = task % NCH;
+      const int64_t row = r0 + ri, j = (int64_t)jt * TJ + c * 32 + lane;
+      return (task < R * NCH && row < m && j < n) ? (int)__ldg(Q + row * n + j) : 0xFF;
+    };
+    int cn[NCODE];
+    if constexpr (PREFETCH) {
+#pragma unroll
+      for (int u = 0; u < NTASK; ++u) cn[u] = (jt_lo < jt_hi) ? load_codes(jt_lo, u) : 0xFF;
+    }
     for (int jt = jt_lo; jt < jt_hi; ++jt) {
       const int64_t J0 = (int64_t)jt * TJ;
+      const int bf = (jt - jt_lo) & 1;
       TP_T0(ta);
-      // (1) sorted order of each row's 32-column chunks (counting sort by code); overlaps MMA
-      constexpr int NTASK = (R * NCH + 7) / 8;
-      constexpr int UB8 = NTASK < 8 ? NTASK : 8;  // tasks whose codes are loaded together
+      // counting sort of each (row, chunk) by code; overlaps the MMAs of this tile
+      int cur[NCODE];
+      if constexpr (PREFETCH) {
 #pragma unroll
-      for (int u0 = 0; u0 < NTASK; u0 += UB8) {
-        int codes[UB8];
-#pragma unroll
-        for (int u = 0; u < UB8; ++u) {
-          const int task = e + 8 * (u0 + u);
-          const int ri = task / NCH, c = task % NCH;
-          const int64_t row = r0 + ri, j = J0 + c * 32 + lane;
-          codes[u] = (task < R * NCH && row < m && j < n) ? (int)__ldg(Q + row * n + j) : 0xFF;
-        }
-#pragma unroll
-        for (int u = 0; u < UB8; ++u) {
-          const int task = e + 8 * (u0 + u);
-          if (task >= R * NCH) break;
-          const int ri = task / NCH, c = task % NCH;
-          const int code = codes[u];
-          const unsigned lt = (1u << lane) - 1u;
-          int base = 0, pos = -1;
-#pragma unroll
-          for (int a = 0; a < NLEV; ++a) {
-            const unsigned bal = __ballot_sync(0xffffffffu, code == a);
-            if (lane == 0) sm.off[ri][c][a] = (uint8_t)base;
-            if (code == a) pos = base + __popc(bal & lt);
-            base += __popc(bal);
-          }
-          if (lane == 0) sm.off[ri][c][NLEV] = (uint8_t)base;
-          // invalid columns (j >= n, rows >= m) go after every segment
-          sm.ipos[ri][c * 32 + lane] = (uint8_t)(pos >= 0 ? pos : 31);
+        for (int u = 0; u < NTASK; ++u) {
+          cur[u] = cn[u];
+          if (jt + 1 < jt_hi) cn[u] = load_codes(jt + 1, u);
         }
       }
-      if (h == 0) sm.scale[et] = (J0 + et < n) ? (float)scale[J0 + et] : 0.0f;
-      named_bar_sync(1, EPI_THREADS);
+#pragma unroll
+      for (int u = 0; u < NTASK; ++u) {
+        const int task = e + 8 * u;
+        if (task >= R * NCH) break;
+        const int ri = task / NCH, c = task % NCH;
+        int code;
+        if constexpr (PREFETCH) code = cur[u];
+        else code = load_codes(jt, u);
+        const unsigned lt = (1u << lane) - 1u;
+        int base = 0, pos = -1;
+#pragma unroll
+        for (int a = 0; a < NLEV; ++a) {
+          const unsigned bal = __ballot_sync(0xffffffffu, code == a);
+          if (code == a) pos = base + __popc(bal & lt);
+          base += __popc(bal);
+          if (lane == 0) sm.oend[bf][ri][c][a] = (uint8_t)base;
+        }
+        // invalid columns (j >= n, rows >= m) go after every segment
+        sm.ipos[bf][ri][c * 32 + lane] = (uint8_t)(pos >= 0 ? pos : 31);
+      }
+      if (h == 0) sm.scale[bf][et] = (J0 + et < n) ? (float)scale[J0 + et] : 0.0f;
+      named_bar_sync(1, EPI_THREADS);  // every warp's sort of this tile is visible
       TP_ACC(e_sort, ta);
       TP_T0(tb0);
       // (2) drain: exact int32 digit sums -> fp32 (* s_j) into the staging tile, release TMEM
@@ -340,11 +435,11 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         tmem_ld16(tb + 2 * TJ, d2);
         // the 16 sorted positions and scales of these columns, loaded before any staging store
         // (vector loads; no shared-memory load waits between the stores)
-        const uint4 ip4 = *reinterpret_cast<const uint4*>(&sm.ipos[i][g * 16]);
+        const uint4 ip4 = *reinterpret_cast<const uint4*>(&sm.ipos[bf][i][g * 16]);
         float sc[16];
 #pragma unroll
         for (int t4 = 0; t4 < 4; ++t4) {
-          const float4 s4 = reinterpret_cast<const float4*>(&sm.scale[g * 16])[t4];
+          const float4 s4 = reinterpret_cast<const float4*>(&sm.scale[bf][g * 16])[t4];
           sc[4 * t4 + 0] = s4.x;
           sc[4 * t4 + 1] = s4.y;
           sc[4 * t4 + 2] = s4.z;
@@ -356,14 +451,19 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         if (small_sums) {
           // |digit sum| <= 128 (n - 1) < 2^22: exact conversion by adding to 1.5 * 2^23 in the
           // integer domain and subtracting it in fp32 (full-rate IADD + FADD instead of I2F)
+          // (paired fp32 arithmetic on two columns at a time: the same bits as scalar code)
+          const float2 mg = make_float2(-12582912.0f, -12582912.0f);  // -1.5 * 2^23
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23 == __int_as_float(0x4B400000)
-            const float f0 = __int_as_float((int)d0[t] + 0x4B400000) - MAGIC;
-            const float f1 = __int_as_float((int)d1[t] + 0x4B400000) - MAGIC;
-            const float f2 = __int_as_float((int)d2[t] + 0x4B400000) - MAGIC;
-            const float v = fmaf(f0, 65536.0f, fmaf(f1, 256.0f, f2));
-            srow[(ipw[t >> 2] >> (8 * (t & 3))) & 0xFF] = v * sc[t];  // sorted order in its chunk
+          for (int t = 0; t < 16; t += 2) {
+            auto cv = [&](uint32_t x) { return __int_as_float((int)x + 0x4B400000); };
+            const float2 f0 = __fadd2_rn(make_float2(cv(d0[t]), cv(d0[t + 1])), mg);
+            const float2 f1 = __fadd2_rn(make_float2(cv(d1[t]), cv(d1[t + 1])), mg);
+            const float2 f2 = __fadd2_rn(make_float2(cv(d2[t]), cv(d2[t + 1])), mg);
+            const float2 v = __fmul2_rn(
+                __ffma2_rn(f0, make_float2(65536.0f, 65536.0f), __ffma2_rn(f1, make_float2(256.0f, 256.0f), f2)),
+                make_float2(sc[t], sc[t + 1]));
+            srow[(ipw[t >> 2] >> (8 * (t & 3))) & 0xFF] = v.x;  // sorted order in its chunk
+            srow[(ipw[(t + 1) >> 2] >> (8 * ((t + 1) & 3))) & 0xFF] = v.y;
           }
         } else {
 #pragma unroll
@@ -376,37 +476,45 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.tempty);  // the next j-tile's MMAs may start now
+      if (lane == 0) {  // the next j-tile's MMAs may start now
+        if (!PAIR || leader) mbar_arrive(&sm.tempty);
+        else mbar_arrive_remote(&sm.tempty, 0);
+      }
       TP_ACC(e_drain, tc0);
       TP_T0(td0);
-      // (3) segment sums over this thread's own (sorted) staging row: prefix sums in place,
-      //     segment a of chunk c = P[off[a+1]] - P[off[a]]
+      // (3) segment sums over this thread's own (sorted) staging row: inclusive prefix sums in
+      //     registers, stored back; segment a of chunk c = P[end_a - 1] - P[end_{a-1} - 1]
 #pragma unroll 1
       for (int c = 2 * h; c < ((dbg & 1) ? 0 : 2 * h + 2); ++c) {
         float* row = &sm.stage[et][c * 32];
         float v[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = row[q];
-        float p = 0.0f;
-        row[0] = 0.0f;
-#pragma unroll
-        for (int q = 0; q < 31; ++q) {
-          p += v[q];
-          row[q + 1] = p;  // P[q + 1]
+        for (int q4 = 0; q4 < 8; ++q4) {
+          const float4 x = reinterpret_cast<const float4*>(row)[q4];
+          v[4 * q4 + 0] = x.x;
+          v[4 * q4 + 1] = x.y;
+          v[4 * q4 + 2] = x.z;
+          v[4 * q4 + 3] = x.w;
         }
-        const float ptot = p + v[31];  // P[32]
+#pragma unroll
+        for (int q = 1; q < 32; ++q) v[q] += v[q - 1];
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          reinterpret_cast<float4*>(row)[q4] = make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+        uint32_t ow[TcSmem<NLEV, STAGES>::NLEVP / 4];
+#pragma unroll
+        for (int w4 = 0; w4 < TcSmem<NLEV, STAGES>::NLEVP / 4; ++w4)
+          ow[w4] = reinterpret_cast<const uint32_t*>(&sm.oend[bf][i][c][0])[w4];
+        float lo = 0.0f;
 #pragma unroll
         for (int a = 0; a < NLEV; ++a) {
-          const int s0 = sm.off[i][c][a], s1 = sm.off[i][c][a + 1];
-          const float hi = (s1 == 32) ? ptot : row[s1];
-          const float lo = row[s0];  // s0 <= 31
-          acc[a] += (s1 > s0) ? (double)(hi - lo) : 0.0;
+          const int s1 = (ow[a >> 2] >> (8 * (a & 3))) & 0xFF;
+          const float hi = (s1 > 0) ? row[s1 - 1] : 0.0f;
+          acc[a] += (double)(hi - lo);
+          lo = hi;
         }
       }
       TP_ACC(e_walk, td0);
-      TP_T0(te0);
-      named_bar_sync(1, EPI_THREADS);  // ipos/off/scale/stage are rewritten for the next j-tile
-      TP_ACC(e_bar, te0);
     }
     {
       long long tot = 0;
@@ -420,6 +528,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     }
     // the two halves' partial sums meet in the (now free) staging tile, in a fixed order
     double* red = reinterpret_cast<double*>(&sm.stage[0][0]);
+    named_bar_sync(1, EPI_THREADS);  // every walk has finished with its staging row
     if (h == 1) {
 #pragma unroll
       for (int a = 0; a < NLEV; ++a) red[et * NLEV + a] = acc[a];
@@ -435,7 +544,10 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   __syncthreads();
   cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == 1) {
+    if (PAIR) tmem_dealloc_pair(tmem, 512);
+    else tmem_dealloc(tmem, 512);
+  }
 }
 
 // Per layer: s_j and the three balanced int8 digits of round(H_jk / s_j) for k < j (else 0).
@@ -505,9 +617,11 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
     return GANQ_ERR_CUDA;
   }
   constexpr int R = 128 / NLEV;
-  const size_t smem = 1024 + STAGES * STAGE_BYTES + sizeof(TcSmem<NLEV>);
-  GANQ_CUDA_TRY(cudaFuncSetAttribute(tgram_tc_kernel<NLEV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+  static const bool pair = getenv("GANQ_TGRAM_PAIR") ? atoi(getenv("GANQ_TGRAM_PAIR")) != 0 : false;
+  auto kern = pair ? tgram_tc_kernel<NLEV, true> : tgram_tc_kernel<NLEV, false>;
+  const size_t smem = pair ? 1024 + TgCfg<true>::STAGES * TgCfg<true>::STAGE_BYTES + sizeof(TcSmem<NLEV, TgCfg<true>::STAGES>)
+                           : 1024 + TgCfg<false>::STAGES * TgCfg<false>::STAGE_BYTES + sizeof(TcSmem<NLEV, TgCfg<false>::STAGES>);
+  GANQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // split the j-tiles (work of tile jt = ktiles_of(jt)) into SPLIT ranges of equal work
   const int NT = (int)((n + TJ - 1) / TJ);
   int64_t total = 0;
@@ -535,7 +649,7 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  GANQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, tgram_tc_kernel<NLEV>, tmap, Q, scale, m, n, P, jsplit, gp, Cg, dbg));
+  GANQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tmap, Q, scale, m, n, P, jsplit, gp, Cg, dbg));
   GANQ_LAUNCH_CHECK("tgram_tc_kernel");
   if (dbg & 16) {
     unsigned long long h[16];
