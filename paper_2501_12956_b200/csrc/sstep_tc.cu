@@ -363,7 +363,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     // barrier), store the codes and quantize finished halves of residuals for the tensor cores.
     // named barriers: the panel end, and per sub-panel parity (the decision warp may run two
     // sub-panels ahead of the helpers and vice versa, so each id has one open phase at most)
-    constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_X = 6, BAR_HELP = 8;  // ES: 4, 5; X: 6, 7
+    constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_HELP = 8, BAR_X = 9;  // ES: 4, 5; X: 9 .. 12
     if (warp == DECIDE_WARP) {
       // ===== decision warp.  The row's codebook sorted (stable by index); th[s] separates
       // sorted positions s and s + 1: the midpoint of two distinct values (a tie goes to the
@@ -423,45 +423,54 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         TP_T0(t1);
         mbar_wait(&sm.ldbar, q & 1);
         TP_ACC(w_ld, t1);
-        float a2[SB];  // feedback of the sub-panel being decided into the next one (sp - 1)
+        // register-carried feedback (the helpers deliver sub-panels three or more to the right):
+        // a2 = into the sub-panel being decided from the two to its right, a3 = into the next one
+        // from the one after it
+        float a2[SB], a3[SB];
+#pragma unroll
+        for (int k = 0; k < SB; ++k) a2[k] = a3[k] = 0.0f;
 #pragma unroll 1
         for (int sp = NSUB - 1; sp >= 0; --sp) {
           const int64_t j0 = jb + SB * sp;  // first column of the sub-panel (may be < 0)
           TP_T0(tb);
-          // the helpers' feedback from sub-panels >= sp + 2 into sp (none for the first two)
-          if (sp < NSUB - 2) named_bar_sync(BAR_X + (sp & 1), PANEL_THREADS);
+          // the helpers' feedback from sub-panels >= sp + 3 into sp (none for the first three)
+          if (sp < NSUB - 3) named_bar_sync(BAR_X + (sp & 3), PANEL_THREADS);
           TP_ACC(c_bar, tb);
           TP_T0(t2);
-          float a[SB], w[SB], tv[SB], lc[SB];
+          float a[SB], w[SB], tv[SB], lc[SB], n1[SB], n2[SB];
 #pragma unroll
           for (int cc = 1; cc < SB; ++cc) lc[cc] = sm.Ld[SB * sp + cc][SB * sp + cc - 1];  // critical path
 #pragma unroll
           for (int k = 0; k < SB; ++k) {
-            a[k] = sm.As[ab][SB * sp + k][lane];
-            if (sp < NSUB - 1) a[k] += a2[k];
-            a2[k] = 0.0f;
+            a[k] = __fadd_rn(sm.As[ab][SB * sp + k][lane], a2[k]);
+            n1[k] = a3[k];  // into sp - 1: from sp + 1 so far, from sp below
+            n2[k] = 0.0f;   // into sp - 2: from sp below
             w[k] = sm.ws[SB * sp + k][lane];
           }
           // the coefficient rows of column cc (in-sub-panel part and next-sub-panel part), loaded
           // one column ahead so that their shared-memory latency is off the decision chain
           TP_ACC(c_ld2, t2);
           TP_T0(t2b);
-          float4 lr[SB / 4], ln[SB / 4];
+          float4 lr[SB / 4], ln[SB / 4], lm[SB / 4];
 #pragma unroll
           for (int k4 = 0; k4 < SB / 4; ++k4) {
             lr[k4] = reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * sp])[k4];
             ln[k4] = (sp > 0) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * (sp - 1)])[k4]
                               : make_float4(0.f, 0.f, 0.f, 0.f);
+            lm[k4] = (sp > 1) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * (sp - 2)])[k4]
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
           for (int cc = SB - 1; cc >= 0; --cc) {
-            float4 lrn[SB / 4], lnn[SB / 4];
+            float4 lrn[SB / 4], lnn[SB / 4], lmn[SB / 4];
             if (cc > 0) {
 #pragma unroll
               for (int k4 = 0; k4 < SB / 4; ++k4) {
                 lrn[k4] = (4 * k4 < cc - 2) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * sp])[k4]
                                             : make_float4(0.f, 0.f, 0.f, 0.f);
                 lnn[k4] = (sp > 0) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * (sp - 1)])[k4]
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                lmn[k4] = (sp > 1) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * (sp - 2)])[k4]
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
               }
             }
@@ -487,27 +496,35 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
                 if (4 * k4 + 3 < cc - 1) a[4 * k4 + 3] = fmaf(ec, l.w, a[4 * k4 + 3]);
               }
             }
-            // ... and into the next sub-panel (paired FMAs)
-            if (sp > 0) {
-              const float2 ee = make_float2(ec, ec);
+            // ... and into the next two sub-panels (paired FMAs)
+            const float2 ee = make_float2(ec, ec);
+            auto fb = [&](const float4 (&l4)[SB / 4], float (&t)[SB]) {
 #pragma unroll
               for (int k4 = 0; k4 < SB / 4; ++k4) {
-                const float4 l = ln[k4];
-                float2 p01 = __ffma2_rn(ee, make_float2(l.x, l.y), make_float2(a2[4 * k4 + 0], a2[4 * k4 + 1]));
-                float2 p23 = __ffma2_rn(ee, make_float2(l.z, l.w), make_float2(a2[4 * k4 + 2], a2[4 * k4 + 3]));
-                a2[4 * k4 + 0] = p01.x;
-                a2[4 * k4 + 1] = p01.y;
-                a2[4 * k4 + 2] = p23.x;
-                a2[4 * k4 + 3] = p23.y;
+                const float4 l = l4[k4];
+                const float2 p01 = __ffma2_rn(ee, make_float2(l.x, l.y), make_float2(t[4 * k4 + 0], t[4 * k4 + 1]));
+                const float2 p23 = __ffma2_rn(ee, make_float2(l.z, l.w), make_float2(t[4 * k4 + 2], t[4 * k4 + 3]));
+                t[4 * k4 + 0] = p01.x;
+                t[4 * k4 + 1] = p01.y;
+                t[4 * k4 + 2] = p23.x;
+                t[4 * k4 + 3] = p23.y;
               }
-            }
+            };
+            if (sp > 0) fb(ln, n1);
+            if (sp > 1) fb(lm, n2);
             if (cc > 0) {
 #pragma unroll
               for (int k4 = 0; k4 < SB / 4; ++k4) {
                 lr[k4] = lrn[k4];
                 ln[k4] = lnn[k4];
+                lm[k4] = lmn[k4];
               }
             }
+          }
+#pragma unroll
+          for (int k = 0; k < SB; ++k) {
+            a2[k] = n1[k];
+            a3[k] = n2[k];
           }
 #pragma unroll
           for (int cc = 0; cc < SB; ++cc) sm.es[SB * sp + cc][lane] = tv[cc];  // the chosen levels
@@ -531,7 +548,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       tp_flush(dbg, lane, 15, c_bar);
     } else {
       // ===== helpers: lane = row.  After sub-panel sp is decided, its residuals are applied to
-      // every column of sub-panels <= sp - 2 (4-column chunks dealt round-robin to the warps);
+      // every column of sub-panels <= sp - 3 (4-column chunks dealt round-robin to the warps);
       // codes leave in 32-column groups, residual digits in 64-column halves.
       const int hw = helper_index(warp);
       const int rr = lane;
@@ -580,21 +597,21 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           }
           named_bar_sync(BAR_HELP, NHELP * 32);
           TP_T0(t4);
-          if (sp >= 2) {
+          if (sp >= 3) {
             float e8[SB];
 #pragma unroll
             for (int cc = 0; cc < SB; ++cc) e8[cc] = sm.es[SB * sp + cc][rr];
-            const int nch = SB * (sp - 1) / 4;  // 4-column chunks of the columns [0, SB (sp - 1))
-            // chunks in descending order: the two of sub-panel sp - 2 (needed next by the decision
-            // warp) first, then the barrier arrive, then the rest (needed two or more sub-panels
-            // later; a helper handles the same chunks at every step, so their order is kept)
+            const int nch = SB * (sp - 2) / 4;  // 4-column chunks of the columns [0, SB (sp - 2))
+            // chunks in descending order: the two of sub-panel sp - 3 (needed next by the decision
+            // warp) first, then the barrier arrive, then the rest (needed later; a helper handles
+            // the same chunks at every step, so their order is kept)
             const int top = nch - 1 - ((nch - 1 - hw) % NHELP + NHELP) % NHELP;  // largest c4 = hw (mod NHELP)
             bool arrived = false;
 #pragma unroll 1
             for (int c4 = top; c4 >= 0; c4 -= NHELP) {
               if (!arrived && c4 < nch - 2) {
                 __syncwarp();
-                named_bar_arrive(BAR_X + (sp & 1), PANEL_THREADS);  // sub-panel sp - 2 has all its feedback
+                named_bar_arrive(BAR_X + ((sp - 3) & 3), PANEL_THREADS);  // sub-panel sp - 3 has all its feedback
                 arrived = true;
               }
               // paired fp32 FMAs (FFMA2: two independent round-to-nearest FMAs, the same bits)
@@ -614,7 +631,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             }
             if (!arrived) {
               __syncwarp();
-              named_bar_arrive(BAR_X + (sp & 1), PANEL_THREADS);
+              named_bar_arrive(BAR_X + ((sp - 3) & 3), PANEL_THREADS);
             }
           }
           TP_ACC(c_x, t4);

@@ -12,15 +12,16 @@
 // (reading R-14), so the tensor-core sums are EXACT integers: the result is deterministic and
 // independent of summation order.
 //
-// Pipeline (one CTA per (row group, j range); SPLIT CTAs per group over balanced j ranges):
-//   warp 0     TMA: the three digit tiles of H (128 j x 128 k, SWIZZLE_128B) per stage; a stage
-//              of 128 k (12 MMAs) amortises the issuer's per-stage barrier wait and commit, which
-//              cost ~30 % of the MMA rate at 64 k (tools/micro/mma_rate.cu: a try_wait per 6 MMAs
-//              alone takes 64 -> 72 cycles per MMA)
-//   warp 1     MMA issuer (+TMEM owner): 3 int32 accumulators of 128 columns, A from TMEM
-//   warps 2-5  one-hot producers, one per TMEM lane quarter: lane (i,b) builds its 64 bytes
-//              [q_ik == b] per stage in registers and tcgen05.st's them into a TMEM ring
-//              (no shared-memory traffic for A; codes prefetched one stage ahead)
+// Pipeline (one CTA per (row group, j range); SPLIT CTAs per group over balanced j ranges; the
+// two CTAs of a cluster hold consecutive row groups and share every H tile by multicast):
+//   warp 0     TMA: the three digit tiles of H (128 j x 128 k, SWIZZLE_128B) per stage
+//   warp 1     MMA issuer (+TMEM owner): 3 int32 accumulators of 128 columns, A from TMEM; one
+//              elected lane issues a stage's 12 MMAs and its commit in one asm block
+//   warps 2-5  one-hot producers, one per TMEM lane quarter: lane (i,b) builds its 128 bytes
+//              [q_ik == b] per stage in registers and tcgen05.st's them into a TMEM ring.  The
+//              NLEV lanes of a row each load 1/NLEV of the row's codes, PD stages ahead, and
+//              exchange them by shuffles (a global load per stage and lane was the producers'
+//              stall: its latency exceeded one stage)
 //   warps 6-13 epilogue, two warps per lane quarter (one per column half): drain TMEM
 //              (digits -> fp32 * s_j) into a shared staging tile and release the accumulators
 //              at once, then the segment sums overlap the next j-tile's MMAs
@@ -39,6 +40,8 @@ namespace {
 
 constexpr int TJ = 128;          // j per tile (UMMA N)
 constexpr int TK = 128;          // k per stage (128-byte swizzle rows of int8)
+constexpr int B_TILE = TJ * TK;                  // 16 KB digit tile of H
+constexpr int STAGE_BYTES = 3 * B_TILE;          // 48 KB (the one-hot A operand lives in TMEM)
 constexpr int SPLIT = 4;                         // CTAs per row group (balanced j ranges)
 constexpr int CS = 2;                            // cluster: CS row groups share every H tile
 constexpr uint16_t CMASK = (1u << CS) - 1;
@@ -47,29 +50,12 @@ constexpr int THREADS = 448;                     // 14 warps
 constexpr int A_COL0 = 3 * TJ;                   // TMEM: 3 accumulators, then the A ring
 constexpr int A_COLS = TK / 4;                   // 32 columns of 4 int8 per stage
 constexpr int NCH = TJ / 32;                     // 32-column chunks per j-tile (sorting unit)
+constexpr uint32_t IDESC = umma_idesc_u8s8(128, TJ);  // A = one-hot bytes 0 / 1 (u8)
 constexpr double QSCALE = 8388608.0 - 65536.0;   // 2^23 - 2^16: |h_int| bound
 constexpr int SROW = TJ + 4;                     // staging row pitch (16-byte aligned rows)
-
-// Two forms of the contraction (PAIR selects):
-//  * single CTA: M = 128 (i, b) lanes per CTA; the cluster's two CTAs share every H tile by
-//    multicast, each holding all 128 j rows of it (3 x 16 KB per stage, 3 stages);
-//  * CTA pair (cta_group::2): one MMA covers both CTAs' 256 (i, b) lanes; each CTA holds only its
-//    64-row half of the j tile (3 x 8 KB per stage), halving the bytes every SM's shared memory
-//    takes in per MMA, and its one-hot A rows in shared memory (16 KB per stage, written by the
-//    producers with plain stores: no TMEM stores competing with the MMAs' accumulator traffic).
-template <bool PAIR>
-struct TgCfg {
-  static constexpr int STAGES = 3;
-  static constexpr int BROWS = PAIR ? TJ / 2 : TJ;  // j rows of a digit tile in this CTA
-  static constexpr int B_TILE = BROWS * TK;
-  // single CTA: the one-hot A operand lives in a TMEM ring (tcgen05.st); pair: in shared memory
-  // after the three B digit tiles (128 rows x 128 k, K-major SW128), read by the MMA directly
-  static constexpr int A_TILE = PAIR ? 128 * TK : 0;
-  static constexpr int STAGE_BYTES = 3 * B_TILE + A_TILE;
-  static constexpr uint32_t IDESC = umma_idesc_u8s8(PAIR ? 256 : 128, TJ);  // A = one-hot 0 / 1 (u8)
-};
-static_assert(A_COL0 + TgCfg<true>::STAGES * A_COLS <= 512 && A_COL0 + TgCfg<false>::STAGES * A_COLS <= 512,
-              "accumulators and the A ring fit TMEM");
+// pipeline depth: 3 stages; 2 at N = 1, whose sort tables (64 rows) fill the rest of shared memory
+__host__ __device__ constexpr int stages_of(int nlev) { return nlev <= 2 ? 2 : 3; }
+static_assert(A_COL0 + 3 * A_COLS <= 512, "accumulators and the A ring fit TMEM");
 
 // debug-only cycle accounting per warp role: compiled with -DGANQ_KPROF, enabled at run time
 // by GANQ_TGRAM_DBG & 16 (tools/tg_prof.sh); absent from the default build
@@ -85,9 +71,10 @@ __device__ __forceinline__ void tp_flush(int dbg, int lane, int slot, long long 
   if ((dbg & 16) && lane == 0) atomicAdd(&g_tgprof[slot], (unsigned long long)v);
 }
 
-template <int NLEV, int STAGES>
+template <int NLEV>
 struct TcSmem {
   static constexpr int R = 128 / NLEV;
+  static constexpr int STAGES = stages_of(NLEV);
   static constexpr int NLEVP = NLEV < 4 ? 4 : NLEV;
   alignas(16) float stage[128][SROW];         // drained Dt tile (fp32 values), row = (i,b)
   // double-buffered per j-tile (the sort of tile t + 1 runs while other warps walk tile t)
@@ -101,18 +88,17 @@ struct TcSmem {
 __host__ __device__ inline int ktiles_of(int jt) { return (jt * TJ + TJ - 1) / TK + 1; }
 static_assert(TJ % TK == 0, "producers step ktiles_of by TJ / TK");
 
-template <int NLEV, bool PAIR>
+template <int NLEV>
 __global__ void __launch_bounds__(THREADS, 1)
 tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ Q,
                 const double* __restrict__ scale, int64_t m, int64_t n, int64_t P,
                 const int4 jsplit, int gp, double* __restrict__ Cg, int dbg) {
   constexpr int R = 128 / NLEV;
-  using Cfg = TgCfg<PAIR>;
-  constexpr int STAGES = Cfg::STAGES, B_TILE = Cfg::B_TILE, STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr int STAGES = stages_of(NLEV);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  TcSmem<NLEV, STAGES>& sm = *reinterpret_cast<TcSmem<NLEV, STAGES>*>(tiles + STAGES * STAGE_BYTES);
+  TcSmem<NLEV>& sm = *reinterpret_cast<TcSmem<NLEV>*>(tiles + STAGES * STAGE_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // blockIdx.x = part * gp + group (gp = groups rounded up to whole clusters): the CS CTAs of a
@@ -126,32 +112,23 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   const int jt_hi = part == 0 ? jsplit.x : part == 1 ? jsplit.y : part == 2 ? jsplit.z : NT;
   double* Cpart = Cg + (size_t)part * (size_t)m * NLEV * NLEV;
 
-  const uint32_t crank = cluster_ctarank();
-  const bool leader = crank == 0;  // PAIR: the CTA that issues the pair's MMAs
   if (threadIdx.x == 0) {
     prefetch_tmap(&tmap);
     for (int s = 0; s < STAGES; ++s) {
-      if (PAIR) {
-        mbar_init(&sm.full[s], 1 + 8);  // (leader's) TMA bytes of both CTAs + both CTAs' producer warps
-        mbar_init(&sm.empty[s], 1);     // the leader's multicast commit
-      } else {
-        mbar_init(&sm.full[s], 1 + 4);  // TMA bytes (all CS slices) + one arrive per producer warp
-        mbar_init(&sm.empty[s], CS);    // one (multicast) MMA commit from every CTA of the cluster
-      }
+      mbar_init(&sm.full[s], 1 + 4);  // TMA bytes (all CS slices) + one arrive per producer warp
+      mbar_init(&sm.empty[s], CS);    // one (multicast) MMA commit from every CTA of the cluster
     }
     mbar_init(&sm.tfull, 1);
-    mbar_init(&sm.tempty, PAIR ? 16 : 8);  // PAIR: the leader's counts both CTAs' epilogue warps
+    mbar_init(&sm.tempty, 8);
     fence_barrier_init();
   }
-  if (warp == 1) {
-    if (PAIR) tmem_alloc_pair(&sm.tmem_slot, 512);
-    else tmem_alloc(&sm.tmem_slot, 512);
-  }
+  if (warp == 1) tmem_alloc(&sm.tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
-  cluster_sync_all();  // every CTA's barriers exist before any multicast or remote signal
+  cluster_sync_all();  // every CTA's barriers exist before any multicast targets them
   tc_fence_after();
   const uint32_t tmem = sm.tmem_slot;
+  const uint32_t crank = cluster_ctarank();
 
   if (warp == 0) {
     // ---------------- TMA: three digit tiles of H per stage
@@ -166,20 +143,12 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           mbar_wait(&sm.empty[s], ((ks / STAGES) & 1) ^ 1);
           TP_ACC(w_empty, t0);
           uint8_t* st = tiles + s * STAGE_BYTES;
-          const int nl = (dbg & 32) ? 1 : 3;  // debug: load one digit tile only (timing probe)
-          if (PAIR) {
-            // this CTA's 64-row half of each digit tile, counted on the leader's barrier
-            if (leader) mbar_arrive_expect_tx(&sm.full[s], 2 * nl * B_TILE);
-            for (int l = 0; l < nl; ++l)
-              tma_load_2d_pair(st + l * B_TILE, &tmap, &sm.full[s], kt * TK,
-                               (int)(l * P + jt * TJ + crank * SLICE));
-          } else {
-            mbar_arrive_expect_tx(&sm.full[s], nl * B_TILE);
-            // this CTA's slice of j rows of each digit tile, multicast to the whole cluster
-            for (int l = 0; l < nl; ++l)
-              tma_load_2d_mc(st + l * B_TILE + crank * SLICE * TK, &tmap, &sm.full[s], kt * TK,
-                             (int)(l * P + jt * TJ + crank * SLICE), CMASK);
-          }
+          mbar_arrive_expect_tx(&sm.full[s], 3 * B_TILE);
+          // this CTA's slice of j rows of each digit tile, multicast to the whole cluster
+#pragma unroll
+          for (int l = 0; l < 3; ++l)
+            tma_load_2d_mc(st + l * B_TILE + crank * SLICE * TK, &tmap, &sm.full[s], kt * TK,
+                           (int)(l * P + jt * TJ + crank * SLICE), CMASK);
         }
       long long tot = 0;
       TP_ACC(tot, t_all);
@@ -187,79 +156,81 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       tp_flush(dbg, 0, 1, w_empty);
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (the whole warp waits; one elected lane issues each stage;
-    // PAIR: the leader's warp only)
-    if (!PAIR || leader) {
-      TP_T0(t_all);
-      long long w_full = 0, w_tempty = 0;
-      uint32_t s = 0, ph = 0;
-      const uint64_t desc0 = umma_desc_sw128(smem_u32(tiles), 16, 1024);
-      for (int jt = jt_lo; jt < jt_hi; ++jt) {
-        TP_T0(t1);
-        mbar_wait(&sm.tempty, ((jt - jt_lo) & 1) ^ 1);
-        TP_ACC(w_tempty, t1);
+    // ---------------- MMA issuer (the whole warp waits; one elected lane issues each stage)
+    TP_T0(t_all);
+    long long w_full = 0, w_tempty = 0;
+    uint32_t s = 0, ph = 0;
+    const uint64_t desc0 = umma_desc_sw128(smem_u32(tiles), 16, 1024);
+    for (int jt = jt_lo; jt < jt_hi; ++jt) {
+      TP_T0(t1);
+      mbar_wait(&sm.tempty, ((jt - jt_lo) & 1) ^ 1);
+      TP_ACC(w_tempty, t1);
+      tc_fence_after();
+      const int nk = ktiles_of(jt);
+      for (int kt = 0; kt < nk; ++kt) {
+        TP_T0(t0);
+        mbar_wait(&sm.full[s], ph);
+        TP_ACC(w_full, t0);
         tc_fence_after();
-        const int nk = ktiles_of(jt);
-        for (int kt = 0; kt < nk; ++kt) {
-          TP_T0(t0);
-          mbar_wait(&sm.full[s], ph);
-          TP_ACC(w_full, t0);
-          tc_fence_after();
-          __syncwarp();
-          const uint64_t bd = desc0 + (uint64_t)(s * (STAGE_BYTES >> 4));
-          const uint32_t at = tmem + A_COL0 + s * A_COLS;
-          // the commit frees stage s in every CTA of the cluster
-          if (dbg & 8) {
-            if (lane == 0) {
-              if (PAIR) mma_commit_pair_mc(&sm.empty[s], CMASK);
-              else mma_commit_mc(&sm.empty[s], CMASK);
-            }
-          } else if (PAIR) {
-            (void)at;
-            mma_i8_ss_stage12_pair_mc(tmem, bd + (uint64_t)((3 * B_TILE) >> 4), bd, Cfg::IDESC, kt == 0 ? 1u : 0u,
-                                      &sm.empty[s], CMASK);
-          } else {
-            mma_i8_ts_stage12_mc(tmem, at, bd, Cfg::IDESC, kt == 0 ? 1u : 0u, &sm.empty[s], CMASK);
-          }
-          if (++s == STAGES) { s = 0; ph ^= 1; }
-        }
         __syncwarp();
-        if (lane == 0) {
-          if (PAIR) mma_commit_pair_mc(&sm.tfull, CMASK);  // both CTAs' accumulators are ready
-          else mma_commit(&sm.tfull);
-        }
+        // the commit frees stage s in every CTA of the cluster
+        if (!(dbg & 8))
+          mma_i8_ts_stage12_mc(tmem, tmem + A_COL0 + s * A_COLS, desc0 + (uint64_t)(s * (STAGE_BYTES >> 4)),
+                               IDESC, kt == 0 ? 1u : 0u, &sm.empty[s], CMASK);
+        else if (lane == 0)
+          mma_commit_mc(&sm.empty[s], CMASK);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
-      long long tot = 0;
-      TP_ACC(tot, t_all);
-      tp_flush(dbg, lane, 2, tot);
-      tp_flush(dbg, lane, 3, w_full);
-      tp_flush(dbg, lane, 4, w_tempty);
+      __syncwarp();
+      if (lane == 0) mma_commit(&sm.tfull);
     }
+    long long tot = 0;
+    TP_ACC(tot, t_all);
+    tp_flush(dbg, lane, 2, tot);
+    tp_flush(dbg, lane, 3, w_full);
+    tp_flush(dbg, lane, 4, w_tempty);
   } else if (warp < 6) {
-    // ---------------- one-hot producers: TMEM lane (i, b) <- [q_ik == b] for the stage's 64 k
+    // ---------------- one-hot producers: TMEM lane (i, b) <- [q_ik == b] for the stage's 128 k
     // (one warp per lane quarter; kept branch-light: a lone warp per scheduler hides no latency)
     const int pl = (warp & 3) * 32 + lane;  // == TMEM lane (this warp's quarter)
     const int i = pl / NLEV, b = pl % NLEV;
     const int64_t row = r0 + i;
     const uint32_t bb = 0x01010101u * (uint32_t)b;
     const uint8_t* qrow = Q + (row < m ? row : 0) * n;
-    // k-tiles wholly inside [0, n) of a valid row load as 4 x 16 B when rows are 16-byte aligned
-    const int kvec = (row < m && (n & 15) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0)
-                         ? (int)(n / TK) : 0;
-    auto load_codes = [&](int kt, uint4 (&v)[TK / 16]) {
-      if (kt < kvec) {
-        const uint4* src = reinterpret_cast<const uint4*>(qrow + (int64_t)kt * TK);
+    // this lane's share of its row's 128 codes per stage: WPL words at byte offset 4 WPL b
+    constexpr int WPL = 32 / NLEV;
+    constexpr int PD = NLEV >= 8 ? 4 : 2;  // stages whose codes are in flight
+    const int row_lane0 = lane & ~(NLEV - 1);  // the row's first lane in this warp
+    const bool vec = row < m && (n & 15) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
+    auto load_share = [&](int kt, uint32_t (&w)[WPL]) {
+      const int64_t k0 = (int64_t)kt * TK + 4 * WPL * b;
+      if (vec && k0 + 4 * WPL <= n) {
+        if constexpr (WPL == 1) {
+          w[0] = __ldg(reinterpret_cast<const uint32_t*>(qrow + k0));
+        } else if constexpr (WPL == 2) {
+          const uint2 x = __ldg(reinterpret_cast<const uint2*>(qrow + k0));
+          w[0] = x.x;
+          w[1] = x.y;
+        } else {
 #pragma unroll
-        for (int c = 0; c < TK / 16; ++c) v[c] = __ldg(src + c);
+          for (int c = 0; c < WPL / 4; ++c) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(qrow + k0) + c);
+            w[4 * c] = x.x;
+            w[4 * c + 1] = x.y;
+            w[4 * c + 2] = x.z;
+            w[4 * c + 3] = x.w;
+          }
+        }
       } else {
 #pragma unroll
-        for (int c = 0; c < TK / 16; ++c) {
-          uint8_t* vb = reinterpret_cast<uint8_t*>(&v[c]);
+        for (int x = 0; x < WPL; ++x) {
+          uint32_t v = 0;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int64_t k = (int64_t)kt * TK + c * 16 + q;
-            vb[q] = (row < m && k < n) ? qrow[k] : (uint8_t)0xFF;
+          for (int y = 0; y < 4; ++y) {
+            const int64_t k = k0 + 4 * x + y;
+            v |= (uint32_t)((row < m && k < n) ? qrow[k] : (uint8_t)0xFF) << (8 * y);
           }
+          w[x] = v;
         }
       }
     };
@@ -271,82 +242,59 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       const uint32_t y = (x ^ bb) | 0x80808080u;
       return ((0x01010100u - y) & 0x80808080u) >> 7;  // == (~(y - 0x01010101) & 0x80808080) >> 7
     };
+    // two cursors over the (j-tile, k-tile) stages: `use` (stage being produced) and `ld` (the
+    // stage whose codes are loaded next, PD ahead)
     int jt = jt_lo, kt = 0, nk = ktiles_of(jt_lo);
+    int ljt = jt_lo, lkt = 0, lnk = nk;
+    auto load_next = [&](uint32_t (&w)[WPL]) {
+      if (ljt >= jt_hi) return;
+      if (!(dbg & 66)) load_share(lkt, w);  // dbg & 64: timing probe without code loads
+      if (++lkt >= lnk) { ++ljt; lkt = 0; lnk += TJ / TK; }
+    };
     uint32_t s = 0, ph = 0;
     TP_T0(t_all);
     long long w_empty = 0, w_st = 0;
-    // one stage: codes of this stage in cur (loaded a stage ago), prefetch the next into nxt;
-    // build the one-hot words, wait for the slot and issue its TMEM stores (not yet waited on)
-    auto issue = [&](const uint4 (&cur)[TK / 16], uint4 (&nxt)[TK / 16], uint32_t& slot) -> bool {
+    // one stage from the codes in cur; cur is then refilled with the codes PD stages ahead
+    auto stage = [&](uint32_t (&cur)[WPL]) -> bool {
       if (jt >= jt_hi) return false;
-      int jn = jt, kn = kt + 1;
-      if (kn >= nk) { ++jn; kn = 0; }
-      if (jn < jt_hi && !(dbg & 66)) load_codes(kn, nxt);  // dbg & 64: timing probe without code loads
       uint32_t v[TK / 4];
 #pragma unroll
-      for (int c = 0; c < TK / 16; ++c) {
-        v[4 * c + 0] = onehot(cur[c].x);
-        v[4 * c + 1] = onehot(cur[c].y);
-        v[4 * c + 2] = onehot(cur[c].z);
-        v[4 * c + 3] = onehot(cur[c].w);
-      }
+      for (int x = 0; x < TK / 4; ++x)
+        v[x] = onehot(__shfl_sync(0xffffffffu, cur[x % WPL], row_lane0 + x / WPL));
+      load_next(cur);
       TP_T0(t0);
       mbar_wait(&sm.empty[s], ph ^ 1);
       TP_ACC(w_empty, t0);
       tc_fence_after();
-      if (!(dbg & 2)) {
-        if constexpr (PAIR) {
-          // row pl of the stage's A tile, 16-byte chunk c at (c ^ (pl & 7)) (128-byte swizzle)
-          uint8_t* arow = tiles + s * STAGE_BYTES + 3 * B_TILE + pl * TK;
-#pragma unroll
-          for (int c = 0; c < TK / 16; ++c)
-            *reinterpret_cast<uint4*>(arow + ((c ^ (pl & 7)) << 4)) =
-                make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-        } else {
-          const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS;
-#pragma unroll
-          for (int h16 = 0; h16 < TK / 64; ++h16) {
-            uint32_t w16[16];
-#pragma unroll
-            for (int x = 0; x < 16; ++x) w16[x] = v[16 * h16 + x];
-            tmem_st16(ta + 16 * h16, w16);
-          }
-        }
-      }
-      slot = s;
-      if (jn != jt) nk += TJ / TK;  // ktiles_of(jt + 1) = ktiles_of(jt) + TJ / TK
-      jt = jn;
-      kt = kn;
-      if (++s == STAGES) { s = 0; ph ^= 1; }
-      return true;
-    };
-    // publish a stage once its stores are complete (publishing two stages per wait was measured
-    // slower: stage s then waits for stage s + 1's slot)
-    auto publish = [&](uint32_t s0, uint32_t s1, bool two) {
       TP_T0(t2);
-      if constexpr (PAIR) fence_proxy_async_smem();  // generic stores -> the MMA's (async) reads
-      else tmem_st_wait();
+      if (!(dbg & 2)) {
+        const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + A_COL0 + s * A_COLS;
+#pragma unroll
+        for (int h16 = 0; h16 < TK / 64; ++h16) {
+          uint32_t w16[16];
+#pragma unroll
+          for (int x = 0; x < 16; ++x) w16[x] = v[16 * h16 + x];
+          tmem_st16(ta + 16 * h16, w16);
+        }
+        tmem_st_wait();
+      }
       TP_ACC(w_st, t2);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        if (!PAIR || leader) {
-          mbar_arrive(&sm.full[s0]);
-          if (two) mbar_arrive(&sm.full[s1]);
-        } else {  // the leader's MMAs read this CTA's A slots
-          mbar_arrive_remote(&sm.full[s0], 0);
-          if (two) mbar_arrive_remote(&sm.full[s1], 0);
-        }
-      }
+      if (lane == 0) mbar_arrive(&sm.full[s]);
+      if (++kt >= nk) { ++jt; kt = 0; nk += TJ / TK; }
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+      return true;
     };
-    uint4 ca[TK / 16], cb[TK / 16];
-    if (jt < jt_hi) load_codes(kt, ca);
-    for (;;) {
-      uint32_t s0 = 0;
-      if (!issue(ca, cb, s0)) break;
-      publish(s0, 0, false);
-      if (!issue(cb, ca, s0)) break;
-      publish(s0, 0, false);
+    uint32_t cq[PD][WPL];
+#pragma unroll
+    for (int d = 0; d < PD; ++d) load_next(cq[d]);
+    if constexpr (PD == 4) {
+      while (stage(cq[0]) && stage(cq[1]) && stage(cq[2]) && stage(cq[3])) {
+      }
+    } else {
+      while (stage(cq[0]) && stage(cq[1])) {
+      }
     }
     {
       long long tot = 0;
@@ -476,10 +424,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {  // the next j-tile's MMAs may start now
-        if (!PAIR || leader) mbar_arrive(&sm.tempty);
-        else mbar_arrive_remote(&sm.tempty, 0);
-      }
+      if (lane == 0) mbar_arrive(&sm.tempty);  // the next j-tile's MMAs may start now
       TP_ACC(e_drain, tc0);
       TP_T0(td0);
       // (3) segment sums over this thread's own (sorted) staging row: inclusive prefix sums in
@@ -501,9 +446,9 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
 #pragma unroll
         for (int q4 = 0; q4 < 8; ++q4)
           reinterpret_cast<float4*>(row)[q4] = make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
-        uint32_t ow[TcSmem<NLEV, STAGES>::NLEVP / 4];
+        uint32_t ow[TcSmem<NLEV>::NLEVP / 4];
 #pragma unroll
-        for (int w4 = 0; w4 < TcSmem<NLEV, STAGES>::NLEVP / 4; ++w4)
+        for (int w4 = 0; w4 < TcSmem<NLEV>::NLEVP / 4; ++w4)
           ow[w4] = reinterpret_cast<const uint32_t*>(&sm.oend[bf][i][c][0])[w4];
         float lo = 0.0f;
 #pragma unroll
@@ -544,10 +489,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   __syncthreads();
   cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   tc_fence_after();
-  if (warp == 1) {
-    if (PAIR) tmem_dealloc_pair(tmem, 512);
-    else tmem_dealloc(tmem, 512);
-  }
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 // Per layer: s_j and the three balanced int8 digits of round(H_jk / s_j) for k < j (else 0).
@@ -617,10 +559,8 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
     return GANQ_ERR_CUDA;
   }
   constexpr int R = 128 / NLEV;
-  static const bool pair = getenv("GANQ_TGRAM_PAIR") ? atoi(getenv("GANQ_TGRAM_PAIR")) != 0 : false;
-  auto kern = pair ? tgram_tc_kernel<NLEV, true> : tgram_tc_kernel<NLEV, false>;
-  const size_t smem = pair ? 1024 + TgCfg<true>::STAGES * TgCfg<true>::STAGE_BYTES + sizeof(TcSmem<NLEV, TgCfg<true>::STAGES>)
-                           : 1024 + TgCfg<false>::STAGES * TgCfg<false>::STAGE_BYTES + sizeof(TcSmem<NLEV, TgCfg<false>::STAGES>);
+  auto kern = tgram_tc_kernel<NLEV>;
+  const size_t smem = 1024 + (size_t)stages_of(NLEV) * STAGE_BYTES + sizeof(TcSmem<NLEV>);
   GANQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // split the j-tiles (work of tile jt = ktiles_of(jt)) into SPLIT ranges of equal work
   const int NT = (int)((n + TJ - 1) / TJ);
