@@ -361,9 +361,9 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
     // ---------------- panel group: the decision warp (lane = row) and the helpers, which apply
     // the feedback between sub-panels (the next sub-panel's first, handed over by a named
     // barrier), store the codes and quantize finished halves of residuals for the tensor cores.
-    // named barriers: the panel end, and per sub-panel parity (the decision warp may run two
-    // sub-panels ahead of the helpers and vice versa, so each id has one open phase at most)
-    constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_HELP = 8, BAR_X = 9;  // ES: 4, 5; X: 9 .. 12
+    // named barriers: the panel end, and per sub-panel ids mod 4 (the decision warp may run
+    // three sub-panels ahead of the helpers, so each id has one open phase at most)
+    constexpr uint32_t BAR_PANEL = 3, BAR_ES = 4, BAR_HELP = 8, BAR_X = 9;  // ES: 4 .. 7; X: 9 .. 12
     if (warp == DECIDE_WARP) {
       // ===== decision warp.  The row's codebook sorted (stable by index); th[s] separates
       // sorted positions s and s + 1: the midpoint of two distinct values (a tie goes to the
@@ -531,7 +531,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           TP_ACC(c_loop, t2b);
           TP_ACC(c_dec, t2);
           __syncwarp();
-          named_bar_arrive(BAR_ES + (sp & 1), PANEL_THREADS);  // the levels of sub-panel sp are in es
+          named_bar_arrive(BAR_ES + (sp & 3), PANEL_THREADS);  // the levels of sub-panel sp are in es
         }
         TP_T0(t3);
         named_bar_sync(BAR_PANEL, PANEL_THREADS);  // the helpers finished the panel
@@ -583,7 +583,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         mbar_wait(&sm.ldbar, q & 1);
 #pragma unroll 1
         for (int sp = NSUB - 1; sp >= 0; --sp) {
-          named_bar_sync(BAR_ES + (sp & 1), PANEL_THREADS);  // the decision warp finished sub-panel sp
+          named_bar_sync(BAR_ES + (sp & 3), PANEL_THREADS);  // the decision warp finished sub-panel sp
           // codes and residuals of sub-panel sp from the chosen levels (columns dealt round-robin):
           // code = the first index s with T_s == t_q (the decision picks the first member of a
           // run of equal levels); residual e = w - t_q, zero on phantom columns (j < 0)

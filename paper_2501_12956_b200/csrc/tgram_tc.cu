@@ -95,6 +95,8 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
                 const int4 jsplit, int gp, double* __restrict__ Cg, int dbg) {
   constexpr int R = 128 / NLEV;
   constexpr int STAGES = stages_of(NLEV);
+  constexpr int NB = NLEV == 2 ? 1 : NLEV == 4 ? 2 : NLEV == 8 ? 3 : 4;  // code bits
+  static_assert((1 << NB) == NLEV, "levels are a power of two");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* tiles = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -353,17 +355,35 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         int code;
         if constexpr (PREFETCH) code = cur[u];
         else code = load_codes(jt, u);
-        const unsigned lt = (1u << lane) - 1u;
-        int base = 0, pos = -1;
+        // radix ranks from one ballot per code bit: less(x) = #valid lanes with code < x, by
+        // comparing the bits from the top (eq = the lanes whose higher bits equal x's so far)
+        const unsigned vm = __ballot_sync(0xffffffffu, code < NLEV);
+        unsigned bits[NB];
 #pragma unroll
-        for (int a = 0; a < NLEV; ++a) {
-          const unsigned bal = __ballot_sync(0xffffffffu, code == a);
-          if (code == a) pos = base + __popc(bal & lt);
-          base += __popc(bal);
-          if (lane == 0) sm.oend[bf][ri][c][a] = (uint8_t)base;
+        for (int t = 0; t < NB; ++t) bits[t] = __ballot_sync(0xffffffffu, (code >> t) & 1);
+        auto less = [&](int x, unsigned& eq) {
+          eq = vm;
+          int cnt = 0;
+#pragma unroll
+          for (int t = NB - 1; t >= 0; --t) {
+            if ((x >> t) & 1) {
+              cnt += __popc(eq & ~bits[t]);
+              eq &= bits[t];
+            } else {
+              eq &= ~bits[t];
+            }
+          }
+          return cnt;
+        };
+        unsigned eqc;
+        const int lc = less(code < NLEV ? code : 0, eqc);
+        // stable position (equal codes keep column order); invalid columns (j >= n, rows >= m)
+        // go after every segment
+        sm.ipos[bf][ri][c * 32 + lane] = (uint8_t)(code < NLEV ? lc + __popc(eqc & ((1u << lane) - 1u)) : 31);
+        if (lane < NLEV) {  // lane a: the end of level a's segment = #valid codes <= a
+          unsigned e2;
+          sm.oend[bf][ri][c][lane] = (uint8_t)(lane + 1 < NLEV ? less(lane + 1, e2) : __popc(vm));
         }
-        // invalid columns (j >= n, rows >= m) go after every segment
-        sm.ipos[bf][ri][c * 32 + lane] = (uint8_t)(pos >= 0 ? pos : 31);
       }
       if (h == 0) sm.scale[bf][et] = (J0 + et < n) ? (float)scale[J0 + et] : 0.0f;
       named_bar_sync(1, EPI_THREADS);  // every warp's sort of this tile is visible
