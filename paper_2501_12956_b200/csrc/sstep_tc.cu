@@ -30,6 +30,7 @@
 #include <stdlib.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "ganq_internal.cuh"
 
@@ -429,9 +430,10 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
         float a2[SB], a3[SB];
 #pragma unroll
         for (int k = 0; k < SB; ++k) a2[k] = a3[k] = 0.0f;
-#pragma unroll 1
-        for (int sp = NSUB - 1; sp >= 0; --sp) {
-          const int64_t j0 = jb + SB * sp;  // first column of the sub-panel (may be < 0)
+        // one sub-panel; TL = what is known of sp at compile time (2: sp >= 2, 1: sp == 1, 0: sp == 0),
+        // so that the feedback into the next two sub-panels needs no run-time branch
+        auto subpanel = [&](const int sp, auto tail) {
+          constexpr int TL = decltype(tail)::value;
           TP_T0(tb);
           // the helpers' feedback from sub-panels >= sp + 3 into sp (none for the first three)
           if (sp < NSUB - 3) named_bar_sync(BAR_X + (sp & 3), PANEL_THREADS);
@@ -455,9 +457,9 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
 #pragma unroll
           for (int k4 = 0; k4 < SB / 4; ++k4) {
             lr[k4] = reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * sp])[k4];
-            ln[k4] = (sp > 0) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * (sp - 1)])[k4]
+            ln[k4] = (TL >= 1) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * (sp - 1)])[k4]
                               : make_float4(0.f, 0.f, 0.f, 0.f);
-            lm[k4] = (sp > 1) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * (sp - 2)])[k4]
+            lm[k4] = (TL >= 2) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + SB - 1][SB * (sp - 2)])[k4]
                               : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
@@ -468,9 +470,9 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
               for (int k4 = 0; k4 < SB / 4; ++k4) {
                 lrn[k4] = (4 * k4 < cc - 2) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * sp])[k4]
                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-                lnn[k4] = (sp > 0) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * (sp - 1)])[k4]
+                lnn[k4] = (TL >= 1) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * (sp - 1)])[k4]
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                lmn[k4] = (sp > 1) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * (sp - 2)])[k4]
+                lmn[k4] = (TL >= 2) ? reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc - 1][SB * (sp - 2)])[k4]
                                    : make_float4(0.f, 0.f, 0.f, 0.f);
               }
             }
@@ -510,8 +512,8 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
                 t[4 * k4 + 3] = p23.y;
               }
             };
-            if (sp > 0) fb(ln, n1);
-            if (sp > 1) fb(lm, n2);
+            if constexpr (TL >= 1) fb(ln, n1);
+            if constexpr (TL >= 2) fb(lm, n2);
             if (cc > 0) {
 #pragma unroll
               for (int k4 = 0; k4 < SB / 4; ++k4) {
@@ -532,7 +534,11 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           TP_ACC(c_dec, t2);
           __syncwarp();
           named_bar_arrive(BAR_ES + (sp & 3), PANEL_THREADS);  // the levels of sub-panel sp are in es
-        }
+        };
+#pragma unroll 1
+        for (int sp = NSUB - 1; sp >= 2; --sp) subpanel(sp, std::integral_constant<int, 2>{});
+        subpanel(1, std::integral_constant<int, 1>{});
+        subpanel(0, std::integral_constant<int, 0>{});
         TP_T0(t3);
         named_bar_sync(BAR_PANEL, PANEL_THREADS);  // the helpers finished the panel
         TP_ACC(c_bar, t3);
@@ -606,33 +612,46 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             // warp) first, then the barrier arrive, then the rest (needed later; a helper handles
             // the same chunks at every step, so their order is kept)
             const int top = nch - 1 - ((nch - 1 - hw) % NHELP + NHELP) % NHELP;  // largest c4 = hw (mod NHELP)
-            bool arrived = false;
-#pragma unroll 1
-            for (int c4 = top; c4 >= 0; c4 -= NHELP) {
-              if (!arrived && c4 < nch - 2) {
-                __syncwarp();
-                named_bar_arrive(BAR_X + ((sp - 3) & 3), PANEL_THREADS);  // sub-panel sp - 3 has all its feedback
-                arrived = true;
+            // NC chunks at a time (independent FMA chains interleave); paired fp32 FMAs (FFMA2: two
+            // independent round-to-nearest FMAs, the same bits as scalar code)
+            auto apply = [&](int c4x, auto ncc) {
+              constexpr int NC = decltype(ncc)::value;
+              float2 ac[NC][2];
+#pragma unroll
+              for (int u = 0; u < NC; ++u) {
+                const int c4 = c4x - u * NHELP;
+                ac[u][0] = make_float2(sm.As[ab][4 * c4][rr], sm.As[ab][4 * c4 + 1][rr]);
+                ac[u][1] = make_float2(sm.As[ab][4 * c4 + 2][rr], sm.As[ab][4 * c4 + 3][rr]);
               }
-              // paired fp32 FMAs (FFMA2: two independent round-to-nearest FMAs, the same bits)
-              float2 a01 = make_float2(sm.As[ab][4 * c4][rr], sm.As[ab][4 * c4 + 1][rr]);
-              float2 a23 = make_float2(sm.As[ab][4 * c4 + 2][rr], sm.As[ab][4 * c4 + 3][rr]);
 #pragma unroll
               for (int cc = 0; cc < SB; ++cc) {
-                const float4 l = *reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][4 * c4]);
                 const float2 ee = make_float2(e8[cc], e8[cc]);
-                a01 = __ffma2_rn(ee, make_float2(l.x, l.y), a01);
-                a23 = __ffma2_rn(ee, make_float2(l.z, l.w), a23);
+#pragma unroll
+                for (int u = 0; u < NC; ++u) {
+                  const float4 l = *reinterpret_cast<const float4*>(&sm.Ld[SB * sp + cc][4 * (c4x - u * NHELP)]);
+                  ac[u][0] = __ffma2_rn(ee, make_float2(l.x, l.y), ac[u][0]);
+                  ac[u][1] = __ffma2_rn(ee, make_float2(l.z, l.w), ac[u][1]);
+                }
               }
-              sm.As[ab][4 * c4][rr] = a01.x;
-              sm.As[ab][4 * c4 + 1][rr] = a01.y;
-              sm.As[ab][4 * c4 + 2][rr] = a23.x;
-              sm.As[ab][4 * c4 + 3][rr] = a23.y;
+#pragma unroll
+              for (int u = 0; u < NC; ++u) {
+                const int c4 = c4x - u * NHELP;
+                sm.As[ab][4 * c4][rr] = ac[u][0].x;
+                sm.As[ab][4 * c4 + 1][rr] = ac[u][0].y;
+                sm.As[ab][4 * c4 + 2][rr] = ac[u][1].x;
+                sm.As[ab][4 * c4 + 3][rr] = ac[u][1].y;
+              }
+            };
+            int c4 = top;
+            if (c4 >= nch - 2) {  // this helper's chunk of sub-panel sp - 3 (at most one), first
+              apply(c4, std::integral_constant<int, 1>{});
+              c4 -= NHELP;
             }
-            if (!arrived) {
-              __syncwarp();
-              named_bar_arrive(BAR_X + ((sp - 3) & 3), PANEL_THREADS);
-            }
+            __syncwarp();
+            named_bar_arrive(BAR_X + ((sp - 3) & 3), PANEL_THREADS);  // sub-panel sp - 3 has all its feedback
+#pragma unroll 1
+            for (; c4 - NHELP >= 0; c4 -= 2 * NHELP) apply(c4, std::integral_constant<int, 2>{});
+            if (c4 >= 0) apply(c4, std::integral_constant<int, 1>{});
           }
           TP_ACC(c_x, t4);
           TP_T0(t5);

@@ -313,9 +313,16 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
     const int et = quarter * 32 + lane;    // 0..127 == TMEM lane == (i, b)
     const int i = et / NLEV, b = et % NLEV;
     constexpr int EPI_THREADS = 256;
+    // segment sums collect in fp32 over FLUSH j-tiles (8 chunk segments), then in fp64: the
+    // fp64 pipe (F2F.F64 + DADD per segment) throttled the walk
+    constexpr int FLUSH = 4;
     double acc[NLEV];
+    float acf[NLEV];
 #pragma unroll
-    for (int a = 0; a < NLEV; ++a) acc[a] = 0.0;
+    for (int a = 0; a < NLEV; ++a) {
+      acc[a] = 0.0;
+      acf[a] = 0.0f;
+    }
     TP_T0(t_all);
     long long e_sort = 0, e_wait = 0, e_drain = 0, e_walk = 0, e_bar = 0;  // e_bar: unused
     // (1) codes of a j-tile: task u of this warp = (row ri, 32-column chunk c); prefetched one
@@ -395,26 +402,22 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       TP_T0(tc0);
       tc_fence_after();
 #pragma unroll 1
-      for (int g = h * (TJ / 32); g < ((dbg & 4) ? 0 : (h + 1) * (TJ / 32)); ++g) {
-        uint32_t d0[16], d1[16], d2[16];
-        const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + g * 16;
-        tmem_ld16(tb, d0);
-        tmem_ld16(tb + TJ, d1);
-        tmem_ld16(tb + 2 * TJ, d2);
-        // the 16 sorted positions and scales of these columns, loaded before any staging store
+      // 8 columns at a time (3 x 8 accumulator words in registers)
+      constexpr int DW = 8;
+      for (int g = h * (TJ / 2 / DW); g < ((dbg & 4) ? 0 : (h + 1) * (TJ / 2 / DW)); ++g) {
+        uint32_t d0[DW], d1[DW], d2[DW];
+        const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + g * DW;
+        tmem_ld8(tb, d0);
+        tmem_ld8(tb + TJ, d1);
+        tmem_ld8(tb + 2 * TJ, d2);
+        // the sorted positions and scales of these columns, loaded before any staging store
         // (vector loads; no shared-memory load waits between the stores)
-        const uint4 ip4 = *reinterpret_cast<const uint4*>(&sm.ipos[bf][i][g * 16]);
-        float sc[16];
-#pragma unroll
-        for (int t4 = 0; t4 < 4; ++t4) {
-          const float4 s4 = reinterpret_cast<const float4*>(&sm.scale[bf][g * 16])[t4];
-          sc[4 * t4 + 0] = s4.x;
-          sc[4 * t4 + 1] = s4.y;
-          sc[4 * t4 + 2] = s4.z;
-          sc[4 * t4 + 3] = s4.w;
-        }
-        const uint32_t ipw[4] = {ip4.x, ip4.y, ip4.z, ip4.w};
-        float* srow = &sm.stage[et][(g * 16) & ~31];
+        const uint2 ip2 = *reinterpret_cast<const uint2*>(&sm.ipos[bf][i][g * DW]);
+        const float4 sa = reinterpret_cast<const float4*>(&sm.scale[bf][g * DW])[0];
+        const float4 sb = reinterpret_cast<const float4*>(&sm.scale[bf][g * DW])[1];
+        const float sc[DW] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+        const uint32_t ipw[2] = {ip2.x, ip2.y};
+        float* srow = &sm.stage[et][(g * DW) & ~31];
         tmem_ld_wait();
         if (small_sums) {
           // |digit sum| <= 128 (n - 1) < 2^22: exact conversion by adding to 1.5 * 2^23 in the
@@ -422,7 +425,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           // (paired fp32 arithmetic on two columns at a time: the same bits as scalar code)
           const float2 mg = make_float2(-12582912.0f, -12582912.0f);  // -1.5 * 2^23
 #pragma unroll
-          for (int t = 0; t < 16; t += 2) {
+          for (int t = 0; t < DW; t += 2) {
             auto cv = [&](uint32_t x) { return __int_as_float((int)x + 0x4B400000); };
             const float2 f0 = __fadd2_rn(make_float2(cv(d0[t]), cv(d0[t + 1])), mg);
             const float2 f1 = __fadd2_rn(make_float2(cv(d1[t]), cv(d1[t + 1])), mg);
@@ -435,7 +438,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           }
         } else {
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
+          for (int t = 0; t < DW; ++t) {
             const float v = fmaf((float)(int)d0[t], 65536.0f,
                                  fmaf((float)(int)d1[t], 256.0f, (float)(int)d2[t]));
             srow[(ipw[t >> 2] >> (8 * (t & 3))) & 0xFF] = v * sc[t];
@@ -475,8 +478,15 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         for (int a = 0; a < NLEV; ++a) {
           const int s1 = (ow[a >> 2] >> (8 * (a & 3))) & 0xFF;
           const float hi = (s1 > 0) ? row[s1 - 1] : 0.0f;
-          acc[a] += (double)(hi - lo);
+          acf[a] += hi - lo;
           lo = hi;
+        }
+      }
+      if ((jt - jt_lo) % FLUSH == FLUSH - 1 || jt + 1 == jt_hi) {
+#pragma unroll
+        for (int a = 0; a < NLEV; ++a) {
+          acc[a] += (double)acf[a];
+          acf[a] = 0.0f;
         }
       }
       TP_ACC(e_walk, td0);
