@@ -78,7 +78,7 @@ struct TcSmem {
   static constexpr int NLEVP = NLEV < 4 ? 4 : NLEV;
   alignas(16) float stage[128][SROW];         // drained Dt tile (fp32 values), row = (i,b)
   // double-buffered per j-tile (the sort of tile t + 1 runs while other warps walk tile t)
-  alignas(16) uint8_t ipos[2][R][TJ];         // per (row, 32-chunk): sorted position of each j
+  alignas(16) uint8_t perm[2][R][TJ];         // per (row, 32-chunk): the column at each sorted slot
   alignas(16) float scale[2][TJ];             // s_j of the j-tile (fp32)
   alignas(16) uint8_t oend[2][R][NCH][NLEVP]; // end of each level's segment per (row, chunk)
   alignas(8) uint64_t full[STAGES], empty[STAGES], tfull, tempty;
@@ -386,7 +386,8 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
         const int lc = less(code < NLEV ? code : 0, eqc);
         // stable position (equal codes keep column order); invalid columns (j >= n, rows >= m)
         // go after every segment
-        sm.ipos[bf][ri][c * 32 + lane] = (uint8_t)(code < NLEV ? lc + __popc(eqc & ((1u << lane) - 1u)) : 31);
+        // (slots past the valid count are never part of a segment: left unwritten)
+        if (code < NLEV) sm.perm[bf][ri][c * 32 + lc + __popc(eqc & ((1u << lane) - 1u))] = (uint8_t)lane;
         if (lane < NLEV) {  // lane a: the end of level a's segment = #valid codes <= a
           unsigned e2;
           sm.oend[bf][ri][c][lane] = (uint8_t)(lane + 1 < NLEV ? less(lane + 1, e2) : __popc(vm));
@@ -401,23 +402,21 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
       TP_ACC(e_wait, tb0);
       TP_T0(tc0);
       tc_fence_after();
-#pragma unroll 1
       // 8 columns at a time (3 x 8 accumulator words in registers)
       constexpr int DW = 8;
+#pragma unroll 1
       for (int g = h * (TJ / 2 / DW); g < ((dbg & 4) ? 0 : (h + 1) * (TJ / 2 / DW)); ++g) {
         uint32_t d0[DW], d1[DW], d2[DW];
         const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + g * DW;
         tmem_ld8(tb, d0);
         tmem_ld8(tb + TJ, d1);
         tmem_ld8(tb + 2 * TJ, d2);
-        // the sorted positions and scales of these columns, loaded before any staging store
-        // (vector loads; no shared-memory load waits between the stores)
-        const uint2 ip2 = *reinterpret_cast<const uint2*>(&sm.ipos[bf][i][g * DW]);
+        // the scales of these columns; the values go to the staging row in column order (vector
+        // stores: the walk reads them in sorted order)
         const float4 sa = reinterpret_cast<const float4*>(&sm.scale[bf][g * DW])[0];
         const float4 sb = reinterpret_cast<const float4*>(&sm.scale[bf][g * DW])[1];
         const float sc[DW] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
-        const uint32_t ipw[2] = {ip2.x, ip2.y};
-        float* srow = &sm.stage[et][(g * DW) & ~31];
+        float vv[DW];
         tmem_ld_wait();
         if (small_sums) {
           // |digit sum| <= 128 (n - 1) < 2^22: exact conversion by adding to 1.5 * 2^23 in the
@@ -433,17 +432,17 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
             const float2 v = __fmul2_rn(
                 __ffma2_rn(f0, make_float2(65536.0f, 65536.0f), __ffma2_rn(f1, make_float2(256.0f, 256.0f), f2)),
                 make_float2(sc[t], sc[t + 1]));
-            srow[(ipw[t >> 2] >> (8 * (t & 3))) & 0xFF] = v.x;  // sorted order in its chunk
-            srow[(ipw[(t + 1) >> 2] >> (8 * ((t + 1) & 3))) & 0xFF] = v.y;
+            vv[t] = v.x;
+            vv[t + 1] = v.y;
           }
         } else {
 #pragma unroll
-          for (int t = 0; t < DW; ++t) {
-            const float v = fmaf((float)(int)d0[t], 65536.0f,
-                                 fmaf((float)(int)d1[t], 256.0f, (float)(int)d2[t]));
-            srow[(ipw[t >> 2] >> (8 * (t & 3))) & 0xFF] = v * sc[t];
-          }
+          for (int t = 0; t < DW; ++t)
+            vv[t] = fmaf((float)(int)d0[t], 65536.0f, fmaf((float)(int)d1[t], 256.0f, (float)(int)d2[t])) * sc[t];
         }
+        float4* dst = reinterpret_cast<float4*>(&sm.stage[et][g * DW]);
+        dst[0] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+        dst[1] = make_float4(vv[4], vv[5], vv[6], vv[7]);
       }
       tc_fence_before();
       __syncwarp();
@@ -455,15 +454,13 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
 #pragma unroll 1
       for (int c = 2 * h; c < ((dbg & 1) ? 0 : 2 * h + 2); ++c) {
         float* row = &sm.stage[et][c * 32];
+        // this chunk's values in sorted order (the row's permutation, 32 bytes)
+        const uint4 pa = reinterpret_cast<const uint4*>(&sm.perm[bf][i][c * 32])[0];
+        const uint4 pb = reinterpret_cast<const uint4*>(&sm.perm[bf][i][c * 32])[1];
+        const uint32_t pw[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
         float v[32];
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4) {
-          const float4 x = reinterpret_cast<const float4*>(row)[q4];
-          v[4 * q4 + 0] = x.x;
-          v[4 * q4 + 1] = x.y;
-          v[4 * q4 + 2] = x.z;
-          v[4 * q4 + 3] = x.w;
-        }
+        for (int q = 0; q < 32; ++q) v[q] = row[(pw[q >> 2] >> (8 * (q & 3))) & 31];
 #pragma unroll
         for (int q = 1; q < 32; ++q) v[q] += v[q - 1];
 #pragma unroll
