@@ -135,10 +135,10 @@ def oracle_sample(W_rows: np.ndarray, X_bits: np.ndarray, m: int, p: int, nbits:
                         f"{r}/{m} of its time; layer-equivalent {charged * m / r:.0f} s"))
 
 
-def oracle_inputs(W_cpu: torch.Tensor, X: torch.Tensor, m: int, p: int):
-    """The oracle sample's inputs: ORACLE_ROWS evenly spaced rows of W and the first p r / m
-    tokens of X (bf16 bit patterns)."""
-    r = min(ORACLE_ROWS, m)
+def oracle_inputs(W_cpu: torch.Tensor, X: torch.Tensor, m: int, p: int, rows: int = ORACLE_ROWS):
+    """The oracle sample's inputs: `rows` evenly spaced rows of W and the first p r / m tokens of X
+    (bf16 bit patterns)."""
+    r = min(rows, m)
     rows = np.linspace(0, m - 1, r).astype(int)
     ps = max(1, p * r // m)
     return W_cpu[rows].numpy().astype(np.float64), synthetic.bf16_bits(X[:ps])
@@ -503,9 +503,11 @@ def run_reference(args):
     cfg = synthetic.CONFIGS[args.config]
     m, n, p, nbits, K = cfg["m"], cfg["n"], cfg["p"], cfg["nbits"], cfg["iters"]
     W = synthetic.make_weights(m, n, seed=1000)
-    r = min(ORACLE_ROWS, m)
+    # rows per step: the whole --steps K --warmup W run within about 200 s (the c2 sample costs
+    # ~0.9 s of host time per row on 16 cores), never fewer rows than host cores
+    r = min(m, ORACLE_ROWS, max(cores(), int(200.0 / max(1, args.steps + args.warmup) / 0.9)))
     X = synthetic.make_activations(max(1, p * r // m), n, seed=2000)
-    Wr, Xs = oracle_inputs(W, X, m, p)
+    Wr, Xs = oracle_inputs(W, X, m, p, rows=r)
     for _ in range(args.warmup):
         oracle_sample(Wr, Xs, m, p, nbits, K)
     vals, walls = [], []
@@ -533,7 +535,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 20; 5 for --impl reference, whose steps are host oracle samples)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2", choices=sorted(synthetic.CONFIGS))
@@ -541,6 +544,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-lut", action="store_true", help="skip the NEXT-1 LUT GEMV measurement")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 5 if args.impl == "reference" else 20
     if args.impl == "reference":
         run_reference(args)
     else:
