@@ -336,19 +336,19 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.tempty[buf]);
           }
-          // exact int32 sums -> fp32, combined by weight.  |c0| <= 128^3 = 2^21 and |c1| <= 2^22 (one
-          // and two digit products of 128 u) convert by the add-only 1.5 * 2^23 trick (exact on
-          // [-2^22, 2^22]); |c2| < 3 * 2^21 needs the integer converter.  Paired fp32 arithmetic on
-          // two rows at a time (the same bits as scalar code).
+          // exact int32 sums -> fp32, combined by weight.  |c0| <= 128^3 = 2^21 (one digit product of
+          // 128 u) converts by the add-only 1.5 * 2^23 trick (exact on [-2^22, 2^22]).  Paired fp32
+          // arithmetic on two rows at a time (the same bits as scalar code).
           const float2 mg = make_float2(-12582912.0f, -12582912.0f);
           auto cv = [](uint32_t x) { return __int_as_float((int)x + 0x4B400000); };
+          // (c1 and c2 combine exactly in int32: |256 c1 + c2| < 2^31; one rounding, as the fp32
+          // fma(c1, 256, c2) of the separately converted sums)
 #pragma unroll
           for (int x = 0; x < 16; x += 2) {
             const float2 f0 = __fadd2_rn(make_float2(cv(c0[x]), cv(c0[x + 1])), mg);
-            const float2 f1 = __fadd2_rn(make_float2(cv(c1[x]), cv(c1[x + 1])), mg);
-            const float2 f2 = make_float2((float)(int)c2[x], (float)(int)c2[x + 1]);
-            const float2 v =
-                __ffma2_rn(f0, make_float2(65536.0f, 65536.0f), __ffma2_rn(f1, make_float2(256.0f, 256.0f), f2));
+            const float2 f12 = make_float2((float)((int)c1[x] * 256 + (int)c2[x]),
+                                           (float)((int)c1[x + 1] * 256 + (int)c2[x + 1]));
+            const float2 v = __ffma2_rn(f0, make_float2(65536.0f, 65536.0f), f12);
             const float2 a = __ffma2_rn(v, make_float2(se[16 * hh + x], se[16 * hh + x + 1]),
                                         make_float2(acc[16 * hh + x], acc[16 * hh + x + 1]));
             acc[16 * hh + x] = a.x;

@@ -422,16 +422,18 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
           // |digit sum| <= 128 (n - 1) < 2^22: exact conversion by adding to 1.5 * 2^23 in the
           // integer domain and subtracting it in fp32 (full-rate IADD + FADD instead of I2F)
           // (paired fp32 arithmetic on two columns at a time: the same bits as scalar code)
+          // the low two digits combine exactly in int32 (|256 S1 + S2| < 2^28); its one rounding to
+          // fp32 (the converter, round to nearest) equals the fp32 fma(S1, 256, S2) of the
+          // separately converted digits
           const float2 mg = make_float2(-12582912.0f, -12582912.0f);  // -1.5 * 2^23
 #pragma unroll
           for (int t = 0; t < DW; t += 2) {
             auto cv = [&](uint32_t x) { return __int_as_float((int)x + 0x4B400000); };
             const float2 f0 = __fadd2_rn(make_float2(cv(d0[t]), cv(d0[t + 1])), mg);
-            const float2 f1 = __fadd2_rn(make_float2(cv(d1[t]), cv(d1[t + 1])), mg);
-            const float2 f2 = __fadd2_rn(make_float2(cv(d2[t]), cv(d2[t + 1])), mg);
-            const float2 v = __fmul2_rn(
-                __ffma2_rn(f0, make_float2(65536.0f, 65536.0f), __ffma2_rn(f1, make_float2(256.0f, 256.0f), f2)),
-                make_float2(sc[t], sc[t + 1]));
+            const float2 f12 = make_float2((float)((int)d1[t] * 256 + (int)d2[t]),
+                                           (float)((int)d1[t + 1] * 256 + (int)d2[t + 1]));
+            const float2 v = __fmul2_rn(__ffma2_rn(f0, make_float2(65536.0f, 65536.0f), f12),
+                                        make_float2(sc[t], sc[t + 1]));
             vv[t] = v.x;
             vv[t + 1] = v.y;
           }
