@@ -12,7 +12,7 @@
 // (reading R-14), so the tensor-core sums are EXACT integers: the result is deterministic and
 // independent of summation order.
 //
-// Pipeline (one CTA per (row group, j range); SPLIT CTAs per group over balanced j ranges; the
+// Pipeline (one CTA per (row group, j range); tgram_splits() CTAs per group over balanced j ranges; the
 // two CTAs of a cluster hold consecutive row groups and share every H tile by multicast):
 //   warp 0     TMA: the three digit tiles of H (128 j x 128 k, SWIZZLE_128B) per stage
 //   warp 1     MMA issuer (+TMEM owner): 3 int32 accumulators of 128 columns, A from TMEM; one
@@ -42,7 +42,7 @@ constexpr int TJ = 128;          // j per tile (UMMA N)
 constexpr int TK = 128;          // k per stage (128-byte swizzle rows of int8)
 constexpr int B_TILE = TJ * TK;                  // 16 KB digit tile of H
 constexpr int STAGE_BYTES = 3 * B_TILE;          // 48 KB (the one-hot A operand lives in TMEM)
-constexpr int SPLIT = 4;                         // CTAs per row group (balanced j ranges)
+constexpr int SPLIT = 4;                         // max CTAs per row group (balanced j ranges)
 constexpr int CS = 2;                            // cluster: CS row groups share every H tile
 constexpr uint16_t CMASK = (1u << CS) - 1;
 constexpr int SLICE = TJ / CS;                   // j rows of each digit tile one CTA loads
@@ -92,7 +92,7 @@ template <int NLEV>
 __global__ void __launch_bounds__(THREADS, 1)
 tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ Q,
                 const double* __restrict__ scale, int64_t m, int64_t n, int64_t P,
-                const int4 jsplit, int gp, double* __restrict__ Cg, int dbg) {
+                const int4 jsplit, int nsplit, int gp, double* __restrict__ Cg, int dbg) {
   constexpr int R = 128 / NLEV;
   constexpr int STAGES = stages_of(NLEV);
   constexpr int NB = NLEV == 2 ? 1 : NLEV == 4 ? 2 : NLEV == 8 ? 3 : 4;  // code bits
@@ -111,7 +111,7 @@ tgram_tc_kernel(const __grid_constant__ CUtensorMap tmap, const uint8_t* __restr
   const bool small_sums = n <= 32768;  // every int32 digit sum fits the add-only conversion
   static_assert(SPLIT == 4, "j ranges come from jsplit.x .. z");
   const int jt_lo = part == 0 ? 0 : part == 1 ? jsplit.x : part == 2 ? jsplit.y : jsplit.z;
-  const int jt_hi = part == 0 ? jsplit.x : part == 1 ? jsplit.y : part == 2 ? jsplit.z : NT;
+  const int jt_hi = part + 1 == nsplit ? NT : part == 0 ? jsplit.x : part == 1 ? jsplit.y : jsplit.z;
   double* Cpart = Cg + (size_t)part * (size_t)m * NLEV * NLEV;
 
   if (threadIdx.x == 0) {
@@ -591,15 +591,16 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   auto kern = tgram_tc_kernel<NLEV>;
   const size_t smem = 1024 + (size_t)stages_of(NLEV) * STAGE_BYTES + sizeof(TcSmem<NLEV>);
   GANQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // split the j-tiles (work of tile jt = ktiles_of(jt)) into SPLIT ranges of equal work
+  // split the j-tiles (work of tile jt = ktiles_of(jt)) into nsplit ranges of equal work
+  const int nsplit = tgram_splits();
   const int NT = (int)((n + TJ - 1) / TJ);
   int64_t total = 0;
   for (int jt = 0; jt < NT; ++jt) total += ktiles_of(jt);
-  int bnd[SPLIT - 1];
+  int bnd[SPLIT - 1] = {NT, NT, NT};
   int64_t acc = 0;
   int jt = 0;
-  for (int p = 1; p < SPLIT; ++p) {
-    while (jt < NT && SPLIT * (acc + ktiles_of(jt)) <= p * total) acc += ktiles_of(jt++);
+  for (int p = 1; p < nsplit; ++p) {
+    while (jt < NT && nsplit * (acc + ktiles_of(jt)) <= p * total) acc += ktiles_of(jt++);
     bnd[p - 1] = jt;
   }
   const int4 jsplit = make_int4(bnd[0], bnd[1], bnd[2], 0);
@@ -607,7 +608,7 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   const int gp = (groups + CS - 1) / CS * CS;  // whole clusters; extra CTAs own no rows
   static const int dbg = getenv("GANQ_TGRAM_DBG") ? atoi(getenv("GANQ_TGRAM_DBG")) : 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(SPLIT * gp));
+  cfg.gridDim = dim3((unsigned)(nsplit * gp));
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -618,13 +619,13 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  GANQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tmap, Q, scale, m, n, P, jsplit, gp, Cg, dbg));
+  GANQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, tmap, Q, scale, m, n, P, jsplit, nsplit, gp, Cg, dbg));
   GANQ_LAUNCH_CHECK("tgram_tc_kernel");
   if (dbg & 16) {
     unsigned long long h[16];
     cudaStreamSynchronize(st);
     cudaMemcpyFromSymbol(h, g_tgprof, sizeof(h));
-    const double c = (double)(SPLIT * gp);
+    const double c = (double)(nsplit * gp);
     fprintf(stderr,
             "tgprof per CTA (kcyc): tma %.1f (wait empty %.1f) | mma %.1f (wait full %.1f, tempty %.1f) | "
             "prod/warp %.1f (wait empty %.1f, st %.1f) | epi/warp %.1f (sort %.1f, wait tfull %.1f, drain %.1f, "
@@ -641,6 +642,19 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
 }  // namespace
 
 int64_t tq_pitch(int64_t n) { return (n + 127) / 128 * 128; }
+
+// CTAs per row group of the normal-matrix kernel = the number of partial C blocks tsolve adds.
+// 2 by default: at c2 (512 row groups) 1024 CTAs run in 7 waves of 148 and each CTA's fixed costs
+// (TMEM allocation, pipeline fill, last drain and walk) are spread over twice the tiles of a
+// 4-way split (measured: 1 / 2 / 3 / 4 ways = 12.3 / 11.1 / 11.7 / 11.6 ms per layer)
+int tgram_splits() {
+  static const int s = [] {
+    const char* e = getenv("GANQ_TGRAM_SPLIT");
+    const int v = e ? atoi(e) : 2;
+    return v < 1 ? 1 : v > SPLIT ? SPLIT : v;
+  }();
+  return s;
+}
 
 ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* scale, cudaStream_t st) {
   const int64_t P = tq_pitch(n);

@@ -16,7 +16,7 @@
 namespace ganq {
 namespace {
 
-constexpr int kTgramSplit = 4;  // == SPLIT in tgram_tc.cu
+constexpr int kTgramSplitMax = 4;  // == SPLIT in tgram_tc.cu; tgram_splits() of them are used
 
 // Per row (one warp): D_i[a] = sum_j [q_ij=a] H_jj, b_i[a] = sum_j [q_ij=a] (W H)_ij and the
 // level counts.  Lane l accumulates the columns j = l (mod 32) into its own shared slots
@@ -131,7 +131,7 @@ template <int NLEV>
 __global__ void __launch_bounds__(256)
 tsolve_kernel(double* __restrict__ G, const double* __restrict__ Dv, const double* __restrict__ bvec,
               const int* __restrict__ cnt, int64_t m, int empty_rule, float* __restrict__ T,
-              int* __restrict__ fallback) {
+              int* __restrict__ fallback, int nsplit) {
   constexpr int RPW = 32 / NLEV;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seg = lane / NLEV, l = lane % NLEV;
@@ -158,7 +158,8 @@ tsolve_kernel(double* __restrict__ G, const double* __restrict__ Dv, const doubl
     for (int e = 2 * lane; e < total; e += 64) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int p = 0; p < kTgramSplit; ++p) {
+      for (int p = 0; p < kTgramSplitMax; ++p) {
+        if (p >= nsplit) break;
         const double2 v = *reinterpret_cast<const double2*>(src + p * pstride + e);
         acc.x += v.x;
         acc.y += v.y;
@@ -332,7 +333,8 @@ ganq_status_t launch_tsolve_t(const double* hdiag, const float* WH, const uint8_
                                                                                                Dv, b, cnt);
   GANQ_LAUNCH_CHECK("trhs_kernel");
   tsolve_kernel<NLEV><<<(unsigned)((m + 8 * (32 / NLEV) - 1) / (8 * (32 / NLEV))), 256, 0, st>>>(G, Dv, b, cnt, m,
-                                                                                           empty_rule, T, fb);
+                                                                                           empty_rule, T, fb,
+                                                                                           tgram_splits());
   GANQ_LAUNCH_CHECK("tsolve_kernel");
   tsolve_pinv_kernel<NLEV><<<(unsigned)((m + 127) / 128), 128, 0, st>>>(G, b, cnt, m, empty_rule, T,
                                                                          fb);
