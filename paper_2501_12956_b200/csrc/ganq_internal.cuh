@@ -83,7 +83,7 @@ ganq_status_t launch_sparse_gemm_add(const int64_t* off, const int32_t* col, con
                                      const uint16_t* X, int64_t p, float* Y, cudaStream_t st);
 // tgram_tc.cu
 int64_t tq_pitch(int64_t n);
-int tgram_splits();  // CTAs per row group of the normal-matrix kernel (GANQ_TGRAM_SPLIT, 1..4)
+int tgram_splits(int64_t m, int nlev);  // CTAs per row group of the normal-matrix kernel (1..4)
 ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* scale, cudaStream_t st);
 ganq_status_t launch_tgram_tc(const int8_t* Hq, const double* scale, const uint8_t* Q, int64_t m,
                               int64_t n, int nlev, double* Cg, cudaStream_t st);

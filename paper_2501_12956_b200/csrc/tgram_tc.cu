@@ -592,7 +592,7 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
   const size_t smem = 1024 + (size_t)stages_of(NLEV) * STAGE_BYTES + sizeof(TcSmem<NLEV>);
   GANQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // split the j-tiles (work of tile jt = ktiles_of(jt)) into nsplit ranges of equal work
-  const int nsplit = tgram_splits();
+  const int nsplit = tgram_splits(m, NLEV);
   const int NT = (int)((n + TJ - 1) / TJ);
   int64_t total = 0;
   for (int jt = 0; jt < NT; ++jt) total += ktiles_of(jt);
@@ -644,16 +644,39 @@ ganq_status_t launch_t(const int8_t* Hq, const double* scale, const uint8_t* Q, 
 int64_t tq_pitch(int64_t n) { return (n + 127) / 128 * 128; }
 
 // CTAs per row group of the normal-matrix kernel = the number of partial C blocks tsolve adds.
-// 2 by default: at c2 (512 row groups) 1024 CTAs run in 7 waves of 148 and each CTA's fixed costs
-// (TMEM allocation, pipeline fill, last drain and walk) are spread over twice the tiles of a
-// 4-way split (measured: 1 / 2 / 3 / 4 ways = 12.3 / 11.1 / 11.7 / 11.6 ms per layer)
-int tgram_splits() {
-  static const int s = [] {
+// Each CTA carries fixed costs (TMEM allocation, pipeline fill, the last drain and walk), so fewer
+// and longer CTAs are better as long as the grid still fills whole waves of 148 SMs: the smallest
+// split in 2..4 whose last wave is at least 97 % full, else the fullest (c2: 1024 CTAs in 7 waves;
+// measured at c2: 1 / 2 / 3 / 4 ways = 12.3 / 11.1 / 11.7 / 11.6 ms per layer).  GANQ_TGRAM_SPLIT
+// overrides it.
+int tgram_splits(int64_t m, int nlev) {
+  static const int forced = [] {
     const char* e = getenv("GANQ_TGRAM_SPLIT");
-    const int v = e ? atoi(e) : 2;
-    return v < 1 ? 1 : v > SPLIT ? SPLIT : v;
+    const int v = e ? atoi(e) : 0;
+    return v < 0 ? 0 : v > SPLIT ? SPLIT : v;
   }();
-  return s;
+  if (forced > 0) return forced;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms = v > 0 ? v : 148;
+  }
+  const int64_t groups = (m + 128 / nlev - 1) / (128 / nlev);
+  const int64_t gp = (groups + CS - 1) / CS * CS;
+  int best = SPLIT;
+  double best_fill = 0.0;
+  for (int s2 = 2; s2 <= SPLIT; ++s2) {
+    const double waves = (double)(s2 * gp) / sms;
+    const double fill = waves / (double)((int64_t)((s2 * gp + sms - 1) / sms));
+    if (fill >= 0.97) return s2;
+    if (fill > best_fill) {
+      best_fill = fill;
+      best = s2;
+    }
+  }
+  return best;
 }
 
 ganq_status_t launch_tq_prep(const double* H, int64_t n, int8_t* Hq, double* scale, cudaStream_t st) {

@@ -334,7 +334,7 @@ ganq_status_t launch_tsolve_t(const double* hdiag, const float* WH, const uint8_
   GANQ_LAUNCH_CHECK("trhs_kernel");
   tsolve_kernel<NLEV><<<(unsigned)((m + 8 * (32 / NLEV) - 1) / (8 * (32 / NLEV))), 256, 0, st>>>(G, Dv, b, cnt, m,
                                                                                            empty_rule, T, fb,
-                                                                                           tgram_splits());
+                                                                                           tgram_splits(m, NLEV));
   GANQ_LAUNCH_CHECK("tsolve_kernel");
   tsolve_pinv_kernel<NLEV><<<(unsigned)((m + 127) / 128), 128, 0, st>>>(G, b, cnt, m, empty_rule, T,
                                                                          fb);
