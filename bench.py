@@ -181,8 +181,11 @@ def stage_roofline(name, ms, launches, m, n, p, K, pk, nlev=16):
     if name == "hessian":
         work, unit, bound, peak = n * (n + 1) * p / 1e12, "TFLOP/s", "tensor", pk["bf16"]
     elif name == "tgram":
-        work, unit, bound, peak = K * m * n * (n - 1) / 2 / 1e12, "TFLOP/s", "alu", alu_adds  # 1 FADD = 1 flop
+        # the larger of SURVEY 8(d) G8's FP32-ALU bound (a CUDA-core T-build) and the ceiling of the
+        # one-hot tensor-core formulation used here (the larger at 3 bits): never above 1
         form = 2 * pk["bf16"] / 2 / (3 * nlev)    # int8 MAC/s / (3 nlev MACs per addition)
+        work, unit = K * m * n * (n - 1) / 2 / 1e12, "TFLOP/s"  # 1 addition = 1 flop
+        bound, peak = ("alu", alu_adds) if alu_adds >= form else ("tensor", form)
         extra = {"formulation": "one-hot int8 tcgen05 (R-14)", "formulation_peak": round(form, 3),
                  "formulation_frac": round(work / s / form, 4)}
     elif name == "tsolve":
