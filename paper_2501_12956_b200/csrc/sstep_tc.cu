@@ -71,6 +71,7 @@ struct SsSmem {
   alignas(16) float es[PW][RB + 1];      // residuals of the current panel (column, row)
   alignas(16) uint8_t cs[PW][RB + 4];    // codes of the current panel (column, row)
   alignas(16) float sEn[RB];             // E scales of the newest source panel (rows)
+  alignas(16) float pmx[NHELP][RB];      // per helper: max |e| of the residuals it formed this panel
   alignas(16) float ws[PW][RB + 1];      // weights of the current panel (column, row)
   alignas(8) uint64_t full[STAGES], empty[STAGES], tfull[NBUF], tempty[NBUF];
   alignas(8) uint64_t acc_ready[2], as_free[2], ebar, ldbar;
@@ -593,6 +594,7 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
       named_bar_sync(BAR_PANEL, PANEL_THREADS);
       TP_T0(t_all);
       long long c_x = 0, c_st = 0;
+      float emax = 0.0f;  // max |e| over the residuals this helper formed in the current panel
       for (int q = 0; q < P; ++q) {
         const int64_t jb = n - (int64_t)PW * (q + 1);
         const int ab = q & 1;
@@ -610,7 +612,13 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
 #pragma unroll
             for (int s2 = NLEV - 1; s2 >= 0; --s2) iq = (Tr[s2] == tq) ? s2 : iq;
             sm.cs[SB * sp + cc][rr] = (uint8_t)iq;
-            sm.es[SB * sp + cc][rr] = (jb + SB * sp + cc >= 0) ? __fsub_rn(sm.ws[SB * sp + cc][rr], tq) : 0.0f;
+            const float e = (jb + SB * sp + cc >= 0) ? __fsub_rn(sm.ws[SB * sp + cc][rr], tq) : 0.0f;
+            sm.es[SB * sp + cc][rr] = e;
+            emax = fmaxf(emax, fabsf(e));  // the panel's scale is the max over all helpers' maxima
+          }
+          if (sp == 0) {
+            sm.pmx[hw][rr] = emax;
+            emax = 0.0f;
           }
           named_bar_sync(BAR_HELP, NHELP * 32);
           TP_T0(t4);
@@ -690,11 +698,12 @@ sstep_tc_kernel(const __grid_constant__ CUtensorMap tmLT, const __grid_constant_
           // digits of E (reading R-15) at storage columns j + (npq - n)
           if (hw < 4 && sp == 0 && q < P - 1) {
             // the finished panel (a source of every panel left of it): the row's scale max |e| /
-            // QSCALE over its 128 columns (each helper computes it: the same value) and the
-            // digits; helper hw digitises the 32 columns [32 hw, 32 hw + 32)
-            float mx = 0.0f;
-#pragma unroll 8
-            for (int x = 0; x < PW; ++x) mx = fmaxf(mx, fabsf(sm.es[x][rr]));
+            // QSCALE over its 128 columns (the helpers' running maxima, published before the
+            // helper barrier of sub-panel 0) and the digits; helper hw digitises the 32 columns
+            // [32 hw, 32 hw + 32)
+            float mx = sm.pmx[0][rr];
+#pragma unroll
+            for (int h2 = 1; h2 < NHELP; ++h2) mx = fmaxf(mx, sm.pmx[h2][rr]);
             const float scale = (mx > 0.0f) ? mx / QSCALE : 0.0f;
             const float inv = (mx > 0.0f) ? QSCALE / mx : 0.0f;
             const int64_t hp = npq - n + jb;  // storage column of the panel's first column
