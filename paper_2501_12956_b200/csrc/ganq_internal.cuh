@@ -289,18 +289,6 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// D[tmem] (+)= A[tmem] * B[smem desc], signed int8, exact int32 accumulation (A from TMEM).
-__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 // One pipeline stage of the one-hot T-update contraction, issued by ONE elected lane of a
 // converged warp in a single asm block: for digit l = 0..2 and k-step kk = 0..3,
 //   D[d_tmem + 128 l] (+)= A[a_tmem + 8 kk] * B[bdesc + (l * DIG + 32 kk) bytes]
@@ -353,74 +341,11 @@ __device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(first), "r"(smem_u32(bar)), "h"(mask)                   \
         : "memory");                                                                                     \
   }
-// The same stage with A from shared memory (K-major SW128, 128-byte rows: kk advances the
-// A descriptor by 32 bytes), for a CTA pair: cta_group::2, B digit tiles 8 KB apart.
-__device__ __forceinline__ void mma_i8_ss_stage12_pair_mc(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                                          uint32_t idesc, uint32_t first, uint64_t* bar,
-                                                          uint16_t mask) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred e, acc;\n\t"
-      ".reg .b32 d1, d2;\n\t"
-      ".reg .b64 a, b;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.eq.b32 acc, %4, 0;\n\t"
-      "add.u32 d1, %0, 128;\n\t"
-      "add.u32 d2, %0, 256;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, acc;\n\t"
-      "add.s64 b, %2, 512;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [d1], %1, b, %3, acc;\n\t"
-      "add.s64 b, %2, 1024;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [d2], %1, b, %3, acc;\n\t"
-      "add.s64 a, %1, 2;\n\t"
-      "add.s64 b, %2, 2;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a, b, %3, 1;\n\t"
-      "add.s64 b, %2, 514;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [d1], a, b, %3, 1;\n\t"
-      "add.s64 b, %2, 1026;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [d2], a, b, %3, 1;\n\t"
-      "add.s64 a, %1, 4;\n\t"
-      "add.s64 b, %2, 4;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a, b, %3, 1;\n\t"
-      "add.s64 b, %2, 516;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [d1], a, b, %3, 1;\n\t"
-      "add.s64 b, %2, 1028;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [d2], a, b, %3, 1;\n\t"
-      "add.s64 a, %1, 6;\n\t"
-      "add.s64 b, %2, 6;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], a, b, %3, 1;\n\t"
-      "add.s64 b, %2, 518;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [d1], a, b, %3, 1;\n\t"
-      "add.s64 b, %2, 1030;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::i8 [d2], a, b, %3, 1;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t"
-      "}\n" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(first), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-// descriptor units are 16 bytes: 16 KB = 1024, 8 KB = 512
+// descriptor units are 16 bytes: 16 KB = 1024
 GANQ_STAGE12(mma_i8_ts_stage12_mc, "1", "1024", "2048")
-GANQ_STAGE12(mma_i8_ts_stage12_pair_mc, "2", "512", "1024")
 #undef GANQ_STAGE12
-// shared memory -> TMEM copy of a 128-row x 32-byte matrix (smem descriptor as for an MMA
-// operand) into 8 consecutive TMEM columns of lanes 0-127; ordered with the issuing thread's
-// later tcgen05.mma like any tcgen05 operation of the same thread.
-__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
-  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
-}
 // CTA-pair (cta_group::2) variants: issued by the leader CTA; A rows 0-127 / 128-255 and the
 // two N halves of B live at the same TMEM / shared offsets of the two CTAs.
-__device__ __forceinline__ void mma_i8_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
-                                               uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t"
-      ".reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 __device__ __forceinline__ void mma_commit_pair_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -474,10 +399,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
 }
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
-// Make generic-proxy shared-memory writes visible to the async proxy (tensor core / TMA).
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
