@@ -8,7 +8,7 @@
 // Arithmetic (reading R-12):
 //  * bf16 products are exact in fp32; the tensor core adds them into an fp32 TMEM accumulator.
 //    Its adds truncate (~1 ulp of the accumulator per MMA of K = 16, one-sided), so a chain is
-//    kept to one CHUNK of 512 tokens (32 MMAs); chunks are added into a round-to-nearest fp32
+//    kept to one CHUNK of 256 tokens (16 MMAs); chunks are added into a round-to-nearest fp32
 //    running sum R held in the epilogue's registers.
 //  * Tokens are cut into fixed SUPER-chunks of GANQ_HESSIAN_SUPERCHUNK = 32768 tokens counted from
 //    token 0 of the call.  Each super-chunk's R is stored (fp32) as a PARTIAL; a second kernel

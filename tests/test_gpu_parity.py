@@ -43,9 +43,9 @@ def gpu_H(X):
 
 def p1_check(H, Ho):
     """SURVEY P-1: ||dH||_F / ||H||_F <= 1e-6 and |dH_jk| <= 1e-5 sqrt(H_jj H_kk) (same bf16 X).
-    The GPU's error is the tensor cores' truncating fp32 adds over centred chunks of <= 512 MMAs
-    and one fp32 round-to-nearest fold per chunk (reading R-12); the integer grid adds <= 2^-32 of
-    max|x_j x_k| per super-chunk."""
+    The GPU's error is the tensor cores' truncating fp32 adds over chains of 256 tokens (16 MMAs of
+    K = 16) and one fp32 round-to-nearest fold per chain (reading R-12); the integer grid adds
+    <= 2^-32 of max|x_j x_k| per super-chunk."""
     d = np.sqrt(np.outer(np.diag(Ho), np.diag(Ho)))
     rel = rel_fro(H, Ho)
     el = float(np.max(np.abs(H - Ho) / np.maximum(d, 1e-300)))
